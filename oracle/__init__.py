@@ -1,0 +1,184 @@
+"""CPU oracle for the kernel-map decoder + filter + fusion (arXiv 2202.05977).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_2202_05977_b200``) never imports it, and
+nothing here imports the product package: the two share no code.
+
+The arithmetic lives in ``kmd_oracle.c`` (plain C, fp64, literal Eq. 3 -> 4
+-> 5 of PAPER.md, see the citations there).  This module only builds that
+library with gcc and marshals numpy arrays to it.
+
+Every function is pinned by ``tests/test_oracle_pins.py``; none is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "kmd_oracle.c")
+_HDR = os.path.join(_HERE, "kmd_oracle.h")
+LIB_PATH = os.path.join(_HERE, "libkmd_oracle.so")
+
+_lib = None
+
+_ERRORS = {1: "NULL pointer", 2: "bad config (size/M)", 3: "bad dimension/index", 4: "out of memory"}
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile kmd_oracle.c with gcc (-O2, OpenMP, strict IEEE: no -ffast-math)."""
+    stale = (not os.path.exists(LIB_PATH)) or any(
+        os.path.getmtime(p) > os.path.getmtime(LIB_PATH) for p in (_SRC, _HDR))
+    if force or stale:
+        tmp = LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-Wall", "-Wextra", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        i32 = ctypes.c_int32
+        lib.kmdo_unfold.argtypes = [P, i32, i32, i32, P]
+        lib.kmdo_kernel_map.argtypes = [P, i32, i32, i32, P]
+        lib.kmdo_apply.argtypes = [P, i32, P, i32, i32, P]
+        lib.kmdo_fuse.argtypes = [P, P, i32, i32, i32, i32, P]
+        lib.kmdo_decode_filter_fuse_rows.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
+                                                     i32, i32, i32, P]
+        lib.kmdo_decode_filter_fuse_pixels.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
+                                                       P, P, P, ctypes.c_int64, i32, P]
+        lib.kmdo_max_threads.argtypes = []
+        for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
+                  "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
+                  "kmdo_max_threads"):
+            getattr(lib, f).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise OracleError(f"oracle error {st}: {_ERRORS.get(st, '?')}")
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def max_threads() -> int:
+    return int(_load().kmdo_max_threads())
+
+
+# ---------------------------------------------------------------- explicit path
+def unfold(imap, k: int) -> np.ndarray:
+    """Fig. 3 unfold of an [H,W] map -> [H,W,k*k] (fp64), clamp-to-edge."""
+    imap = _f32(imap)
+    H, W = imap.shape
+    out = np.empty((H, W, k * k), dtype=np.float64)
+    _check(_load().kmdo_unfold(_ptr(imap), H, W, k, _ptr(out)))
+    return out
+
+
+def kernel_map(imap, k: int) -> np.ndarray:
+    """Eq. 3: the explicit H x W x k^2 kernel map (softmax along channels)."""
+    imap = _f32(imap)
+    H, W = imap.shape
+    out = np.empty((H, W, k * k), dtype=np.float64)
+    _check(_load().kmdo_kernel_map(_ptr(imap), H, W, k, _ptr(out)))
+    return out
+
+
+def apply(kmap: np.ndarray, k: int, radiance) -> np.ndarray:
+    """Eq. 4: apply an explicit kernel map to radiance [3,H,W] -> [3,H,W] fp64."""
+    radiance = _f32(radiance)
+    kmap = np.ascontiguousarray(kmap, dtype=np.float64)
+    _, H, W = radiance.shape
+    assert kmap.shape == (H, W, k * k)
+    out = np.empty((3, H, W), dtype=np.float64)
+    _check(_load().kmdo_apply(_ptr(kmap), k, _ptr(radiance), H, W, _ptr(out)))
+    return out
+
+
+def fuse(filtered: np.ndarray, blend, blend_is_logits: bool = True) -> np.ndarray:
+    """Eq. 5: filtered [M,3,H,W] (fp64), blend [M,H,W] (or None iff M==1) -> [3,H,W]."""
+    filtered = np.ascontiguousarray(filtered, dtype=np.float64)
+    M, _, H, W = filtered.shape
+    b = None if blend is None else _f32(blend)
+    out = np.empty((3, H, W), dtype=np.float64)
+    _check(_load().kmdo_fuse(_ptr(filtered), _ptr(b), M, H, W, int(bool(blend_is_logits)),
+                             _ptr(out)))
+    return out
+
+
+def explicit_decode_filter_fuse(radiance, importance, blend, sizes: Sequence[int],
+                                blend_is_logits: bool = True) -> np.ndarray:
+    """KPCN-style composition for ONE frame: materialise every kernel map
+    (unfold -> Eq. 3), apply it (Eq. 4), then fuse (Eq. 5).  Small inputs only."""
+    radiance = _f32(radiance)
+    importance = _f32(importance)
+    M = len(sizes)
+    filtered = np.stack([apply(kernel_map(importance[i], k), k, radiance)
+                         for i, k in enumerate(sizes)])
+    return fuse(filtered, blend if M > 1 else None, blend_is_logits)
+
+
+# --------------------------------------------------------------- streaming path
+def decode_filter_fuse(radiance, importance, blend, sizes: Sequence[int],
+                       blend_is_logits: bool = True, rows: Optional[tuple] = None,
+                       threads: int = 0) -> np.ndarray:
+    """Per-pixel evaluation of Eq. 3 -> 4 -> 5 for radiance [N,3,H,W],
+    importance [N,M,H,W], blend [N,M,H,W] (None iff M==1).  Returns fp64
+    [N,3,H,W], or [N,3,y1-y0,W] for rows=(y0,y1)."""
+    radiance = _f32(radiance)
+    importance = _f32(importance)
+    b = None if blend is None else _f32(blend)
+    N, _, H, W = radiance.shape
+    M = importance.shape[1]
+    assert len(sizes) == M
+    y0, y1 = (0, H) if rows is None else rows
+    sz = np.ascontiguousarray(sizes, dtype=np.int32)
+    out = np.empty((N, 3, y1 - y0, W), dtype=np.float64)
+    _check(_load().kmdo_decode_filter_fuse_rows(
+        _ptr(radiance), _ptr(importance), _ptr(b), N, H, W, M, _ptr(sz),
+        int(bool(blend_is_logits)), y0, y1, threads, _ptr(out)))
+    return out
+
+
+def decode_filter_fuse_pixels(radiance, importance, blend, sizes: Sequence[int],
+                              n, y, x, blend_is_logits: bool = True,
+                              threads: int = 0) -> np.ndarray:
+    """Per-pixel evaluation at the listed (n, y, x) positions -> [count, 3] fp64."""
+    radiance = _f32(radiance)
+    importance = _f32(importance)
+    b = None if blend is None else _f32(blend)
+    N, _, H, W = radiance.shape
+    M = importance.shape[1]
+    assert len(sizes) == M
+    n = np.ascontiguousarray(n, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    sz = np.ascontiguousarray(sizes, dtype=np.int32)
+    out = np.empty((len(n), 3), dtype=np.float64)
+    _check(_load().kmdo_decode_filter_fuse_pixels(
+        _ptr(radiance), _ptr(importance), _ptr(b), N, H, W, M, _ptr(sz),
+        int(bool(blend_is_logits)), _ptr(n), _ptr(y), _ptr(x), len(n), threads, _ptr(out)))
+    return out

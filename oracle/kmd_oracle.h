@@ -1,0 +1,92 @@
+/*
+ * kmd_oracle.h -- plain, slow, obviously-correct CPU oracle for the
+ * kernel-map decoder + per-pixel filtering + kernel fusion of
+ * arXiv 2202.05977 ("weight sharing kernel prediction").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2202_05977_b200/, include/kmd.h) never links,
+ * includes or calls anything here, and nothing here includes the product
+ * headers: the two implementations share no code.
+ *
+ * Arithmetic: fp64 throughout (inputs are fp32, as the GPU path takes them).
+ * Every function follows PAPER.md's equations literally, in the paper's
+ * order (the "explicit kernel map" form of KPCN):
+ *   unfold (Fig. 3)  ->  softmax along the channel axis (Eq. 3)
+ *   -> apply the same weights to R, G, B (Eq. 4)
+ *   -> per-pixel softmax fusion of the M filtered images (Eq. 5).
+ * Readings of points the paper leaves open are DESIGN.md "Readings" R1-R16;
+ * the ones used here: clamp-to-edge sampling for both the unfold and the
+ * colour taps (R1), per-window max subtraction inside the softmax (R2, a
+ * mathematically exact rewrite of Eq. 3), odd sizes only (R3), map i <->
+ * sizes[i] (R4), blend given as logits and softmax-normalised inside (R5).
+ *
+ * Layout (all planar, row-major, contiguous, host memory):
+ *   radiance   [N,3,H,W]  float     noisy demodulated HDR irradiance r(q)
+ *   importance [N,M,H,W]  float     importance maps I_i(q)          (Eq. 2)
+ *   blend      [N,M,H,W]  float     fusion logits (or alphas)       (Eq. 5)
+ *   out        [N,3,rows,W] double  fused result  R^(p)
+ */
+#ifndef KMD_ORACLE_H
+#define KMD_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    KMDO_OK = 0,
+    KMDO_ERR_NULL = 1,    /* a required pointer is NULL                        */
+    KMDO_ERR_CONFIG = 2,  /* even k, k < 1, M < 1, k > min(H,W)                 */
+    KMDO_ERR_DIM = 3,     /* N,H,W < 1 or a row/pixel index out of range        */
+    KMDO_ERR_NOMEM = 4
+};
+
+/* Fig. 3 / PAPER.md:232-234: unfold a single-channel H x W map with a k x k
+ * sliding window.  out[(y*W+x)*k*k + j] = imap[clamp(y+dy), clamp(x+dx)],
+ * offsets (dy,dx) = (j/k - r, j%k - r), r = (k-1)/2, row-major from (-r,-r). */
+int kmdo_unfold(const float* imap, int32_t H, int32_t W, int32_t k, double* out);
+
+/* Eq. 3 + "normalize it with a softmax function along the
+ * channel axis": kmap[(y*W+x)*k*k + j] = w_p(q_j). */
+int kmdo_kernel_map(const float* imap, int32_t H, int32_t W, int32_t k, double* kmap);
+
+/* Eq. 4: R(p,c) = sum_j w_p(q_j) r_c(q_j), the same
+ * weights for each colour channel.  radiance [3,H,W], out [3,H,W]. */
+int kmdo_apply(const double* kmap, int32_t k, const float* radiance,
+               int32_t H, int32_t W, double* out);
+
+/* Eq. 5 with alpha = per-pixel softmax of the M logits
+ * (PAPER.md:251).  filtered [M,3,H,W], blend [M,H,W] (may be NULL iff M==1),
+ * out [3,H,W].  blend_is_logits == 0: blend already holds alpha_i(p). */
+int kmdo_fuse(const double* filtered, const float* blend, int32_t M,
+              int32_t H, int32_t W, int32_t blend_is_logits, double* out);
+
+/* The whole reconstruction (unfold -> Eq. 3 -> Eq. 4 -> Eq. 5) evaluated one
+ * output pixel at a time, each pixel's k x k kernel built on the fly (the
+ * H x W x k^2 map never exists, so full 4K frames fit in host memory).
+ * Computes output rows [y_begin, y_end) of every frame:
+ *   out[((n*3 + c)*(y_end-y_begin) + (y-y_begin))*W + x].
+ * threads <= 0: OpenMP default (all cores of the affinity mask). */
+int kmdo_decode_filter_fuse_rows(const float* radiance, const float* importance,
+                                 const float* blend, int32_t N, int32_t H, int32_t W,
+                                 int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                                 int32_t y_begin, int32_t y_end, int32_t threads,
+                                 double* out);
+
+/* Same, for an explicit list of pixels (frame n[t], row y[t], column x[t]);
+ * out[t*3 + c].  Used to check sampled outputs of full-size frames. */
+int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importance,
+                                   const float* blend, int32_t N, int32_t H, int32_t W,
+                                   int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                                   const int32_t* n, const int32_t* y, const int32_t* x,
+                                   int64_t count, int32_t threads, double* out);
+
+/* Threads OpenMP would use for threads <= 0 (reported as cpu_baseline.cores). */
+int kmdo_max_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,107 @@
+"""Seeded synthetic inputs shaped like the paper's workloads.
+
+This module holds NONE of the method's arithmetic (no unfold, softmax,
+filtering or fusion): it only draws random fields.  It is the one module both
+the CUDA path's tests/bench and the CPU oracle consume (DESIGN.md "Input
+recipe").
+
+Recipe:
+  * radiance r_c = L_c * s_c: the 1-spp noisy demodulated HDR irradiance the
+    paper filters.  L_c = exp(0.75 * smooth_c) is a smooth
+    "clean" signal (~0.1..10), s_c ~ Exp(1) i.i.d. is the 1-spp multiplicative
+    noise surrogate, and fireflies multiply a pixel by 100
+    with probability 1e-4.
+  * importance I_i = 2 * smooth_i + N(0,1): unbounded reals, one map per kernel
+    size, typically in [-10, 10].
+  * blend logits B_i = 1.5 * smooth'_i + N(0, 0.5^2).
+  * smooth = N(0,1) on an (H/32+2) x (W/32+2) grid, bicubic-upsampled to H x W
+    and renormalised to zero mean / unit std.
+Every frame f of a batch is drawn from its own generator seeded with
+``seed + frame_offset + f``, so a batch sharded over ranks is the same set of
+frames as the unsharded batch.
+
+Stress distributions (parity only): "uniform40" (I ~ U(-40,40)), "spikes"
+(sparse +-40 spikes on the paper recipe), "extreme" (I ~ U(-120,120): forces
+the kernels' range fallback), "const" (radiance == 0.5 everywhere).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+import torch.nn.functional as F
+
+BASE_SEED = 220205977
+PAPER_SIZES = (3, 5, 7, 9, 11, 13)  # k_b = 3, k_s = 2, M = 6
+
+DISTS = ("paper", "uniform40", "spikes", "extreme", "const")
+
+
+@dataclass
+class FrameInputs:
+    radiance: torch.Tensor    # [N,3,H,W] fp32
+    importance: torch.Tensor  # [N,M,H,W] fp32
+    blend: Optional[torch.Tensor]  # [N,M,H,W] fp32, None when M == 1 and no blend wanted
+
+
+def _smooth(g: torch.Generator, n: int, H: int, W: int, device) -> torch.Tensor:
+    gh, gw = H // 32 + 2, W // 32 + 2
+    coarse = torch.randn((1, n, gh, gw), generator=g, device=device, dtype=torch.float32)
+    f = F.interpolate(coarse, size=(H, W), mode="bicubic", align_corners=False)[0]
+    f = f - f.mean(dim=(1, 2), keepdim=True)
+    f = f / f.std(dim=(1, 2), keepdim=True).clamp_min(1e-6)
+    return f
+
+
+def _frame(g: torch.Generator, H: int, W: int, M: int, dist: str, with_blend: bool, device):
+    # radiance: smooth signal x Exp(1) noise x rare fireflies
+    L = torch.exp(0.75 * _smooth(g, 3, H, W, device))
+    s = torch.empty((3, H, W), device=device, dtype=torch.float32).exponential_(1.0, generator=g)
+    fire = torch.rand((1, H, W), generator=g, device=device) < 1e-4
+    rad = L * s * torch.where(fire, 100.0, 1.0)
+    if dist == "const":
+        rad = torch.full_like(rad, 0.5)
+    # importance maps
+    if dist in ("paper", "const", "spikes"):
+        imp = 2.0 * _smooth(g, M, H, W, device) + torch.randn((M, H, W), generator=g,
+                                                              device=device)
+        if dist == "spikes":
+            u = torch.rand((M, H, W), generator=g, device=device)
+            imp = torch.where(u < 5e-3, torch.full_like(imp, 40.0), imp)
+            imp = torch.where(u > 1 - 5e-3, torch.full_like(imp, -40.0), imp)
+    elif dist == "uniform40":
+        imp = (torch.rand((M, H, W), generator=g, device=device) * 2 - 1) * 40.0
+    elif dist == "extreme":
+        imp = (torch.rand((M, H, W), generator=g, device=device) * 2 - 1) * 120.0
+    else:
+        raise ValueError(f"unknown dist {dist!r}; expected one of {DISTS}")
+    blend = None
+    if with_blend:
+        blend = 1.5 * _smooth(g, M, H, W, device) + 0.5 * torch.randn((M, H, W), generator=g,
+                                                                      device=device)
+    return rad.contiguous(), imp.contiguous(), blend
+
+
+def make_inputs(N: int, H: int, W: int, M: int, seed: int = BASE_SEED, frame_offset: int = 0,
+                dist: str = "paper", with_blend: Optional[bool] = None,
+                device="cpu") -> FrameInputs:
+    """N frames of (radiance, importance, blend) on ``device`` (fp32, planar)."""
+    if with_blend is None:
+        with_blend = M > 1
+    device = torch.device(device)
+    rads, imps, blends = [], [], []
+    for f in range(N):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed + frame_offset + f)
+        r, i, b = _frame(g, H, W, M, dist, with_blend, device)
+        rads.append(r)
+        imps.append(i)
+        blends.append(b)
+    return FrameInputs(torch.stack(rads), torch.stack(imps),
+                       torch.stack(blends) if with_blend else None)
+
+
+def sizes_from(k_b: int = 3, k_s: int = 2, M: int = 6) -> Sequence[int]:
+    """k_i = k_b + i * k_s."""
+    return tuple(k_b + i * k_s for i in range(M))

@@ -1,0 +1,328 @@
+"""Pins for the CPU oracle (oracle/kmd_oracle.c) against things other than itself.
+
+Each test names what pins it: the paper's equations worked by hand
+(tests/golden), textbook/library routines (scipy box filters), closed forms,
+invariants the equations imply, and a 50-digit brute-force evaluator written
+here independently of the oracle's loop structure.  Chosen so that the likely
+mistakes (a dropped tap, exp(-I), I(p) instead of I(q), transposed dy/dx,
+alpha_i paired with the wrong R_j, wrong clamp) each fail at least one test.
+"""
+import json
+import os
+from fractions import Fraction
+
+import mpmath
+import numpy as np
+import pytest
+from scipy.ndimage import uniform_filter
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RNG = np.random.default_rng(20220205)
+
+
+def _rand_inputs(H, W, M, rng, imp_scale=2.0):
+    rad = rng.exponential(1.0, size=(1, 3, H, W)).astype(np.float32)
+    imp = (imp_scale * rng.standard_normal((1, M, H, W))).astype(np.float32)
+    blend = rng.standard_normal((1, M, H, W)).astype(np.float32)
+    return rad, imp, blend
+
+
+def _box(a, k):
+    """k x k clamp-to-edge box mean (scipy 'nearest' == clamp indexing)."""
+    return uniform_filter(a.astype(np.float64), size=k, mode="nearest")
+
+
+# ----------------------------------------------------------------- unfold (Fig. 3)
+def test_unfold_interior_pixel_is_row_major_neighbourhood(oracle_mod):
+    # SPEC.md:247 example: 5x5 map, k=3, pixel (2,2) -> its 9 neighbours, row-major.
+    imap = np.arange(25, dtype=np.float32).reshape(5, 5)
+    u = oracle_mod.unfold(imap, 3)
+    assert u[2, 2].tolist() == [6, 7, 8, 11, 12, 13, 16, 17, 18]
+
+
+def test_unfold_corner_clamps_to_edge(oracle_mod):
+    imap = np.arange(25, dtype=np.float32).reshape(5, 5)
+    u = oracle_mod.unfold(imap, 3)
+    # (0,0): rows {0,0,1}, cols {0,0,1}
+    assert u[0, 0].tolist() == [0, 0, 1, 0, 0, 1, 5, 5, 6]
+    # (4,2): rows {3,4,4}, cols {1,2,3}
+    assert u[4, 2].tolist() == [16, 17, 18, 21, 22, 23, 21, 22, 23]
+
+
+def test_unfold_k1_and_constant(oracle_mod):
+    imap = RNG.standard_normal((6, 7)).astype(np.float32)
+    assert np.array_equal(oracle_mod.unfold(imap, 1)[..., 0], imap.astype(np.float64))
+    c = np.full((6, 7), 0.375, np.float32)
+    assert np.all(oracle_mod.unfold(c, 5) == 0.375)
+
+
+# ---------------------------------------------------------------- softmax (Eq. 3)
+def test_kernel_map_constant_importance_is_uniform(oracle_mod):
+    km = oracle_mod.kernel_map(np.full((7, 9), -3.25, np.float32), 3)
+    assert np.allclose(km, 1.0 / 9.0, rtol=0, atol=1e-16)
+
+
+def test_kernel_map_dominant_neighbour(oracle_mod):
+    # a neighbour 40 above the rest takes > 1 - 1e-10 of the weight.
+    imap = np.zeros((5, 5), np.float32)
+    imap[1, 3] = 40.0
+    km = oracle_mod.kernel_map(imap, 3)
+    # for pixel (2,2), tap (1,3) is offset (-1,+1) -> j = 0*3 + 2 = 2
+    assert km[2, 2, 2] > 1 - 1e-10
+    # Eq. 3 orientation: the weight follows I(q), not I(p): pixel (1,3)'s own
+    # window has the spike at its centre tap j = 4.
+    assert km[1, 3, 4] > 1 - 1e-10
+
+
+def test_kernel_map_matches_closed_form_exp_ratio(oracle_mod):
+    imap = RNG.uniform(-3, 3, (6, 8)).astype(np.float32)
+    km = oracle_mod.kernel_map(imap, 5)
+    assert np.allclose(km.sum(-1), 1.0, rtol=0, atol=1e-14)
+    e = np.exp(oracle_mod.unfold(imap, 5))
+    assert np.allclose(km, e / e.sum(-1, keepdims=True), rtol=1e-14, atol=0)
+    assert km.min() >= 0 and km.max() <= 1
+
+
+# ------------------------------------------------------------ Eq. 3 + Eq. 4 pins
+@pytest.mark.parametrize("k", [1, 3, 5, 7, 13])
+def test_uniform_importance_is_scipy_box_filter(oracle_mod, k):
+    # Constant I makes every weight 1/k^2, so Eq. 4 is the k x k box mean.
+    H, W = 17, 23
+    rad = RNG.exponential(1.0, (1, 3, H, W)).astype(np.float32)
+    imp = np.full((1, 1, H, W), 1.5, np.float32)
+    out = oracle_mod.decode_filter_fuse(rad, imp, None, [k])[0]
+    for c in range(3):
+        np.testing.assert_allclose(out[c], _box(rad[0, c], k), rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("k", [3, 5, 9, 13])
+def test_ratio_of_box_filters_identity(oracle_mod, k):
+    # Eq. 3 weights depend on q only, so R = box(e*r) / box(e), e = exp(I):
+    # an independent closed form evaluated with scipy's box filter.
+    H, W = 19, 29  # H != W catches transposed dy/dx
+    rad = RNG.exponential(1.0, (1, 3, H, W)).astype(np.float32)
+    imp = RNG.uniform(-4, 4, (1, 1, H, W)).astype(np.float32)
+    out = oracle_mod.decode_filter_fuse(rad, imp, None, [k])[0]
+    e = np.exp(imp[0, 0].astype(np.float64))
+    den = _box(e, k)
+    for c in range(3):
+        ref = _box(e * rad[0, c].astype(np.float64), k) / den
+        np.testing.assert_allclose(out[c], ref, rtol=1e-12, atol=0)
+
+
+def test_k1_is_identity_exactly(oracle_mod):
+    rad, imp, _ = _rand_inputs(9, 11, 1, RNG)
+    out = oracle_mod.decode_filter_fuse(rad, imp, None, [1])
+    assert np.array_equal(out.astype(np.float32), rad)
+
+
+def test_constant_radiance_reproduced_exactly(oracle_mod):
+    # sum_q w_p(q) = 1, so a constant image is reproduced (fp64 then fp32 rounding).
+    H, W = 14, 15
+    rad = np.full((1, 3, H, W), 0.3712, np.float32)
+    _, imp, blend = _rand_inputs(H, W, 3, RNG, imp_scale=5.0)
+    out = oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 7, 13])
+    assert np.array_equal(out.astype(np.float32), rad)
+
+
+def test_convex_hull_of_window(oracle_mod):
+    H, W, k = 12, 13, 5
+    rad, imp, _ = _rand_inputs(H, W, 1, RNG, imp_scale=4.0)
+    out = oracle_mod.decode_filter_fuse(rad, imp, None, [k])[0]
+    from scipy.ndimage import maximum_filter, minimum_filter
+    for c in range(3):
+        lo = minimum_filter(rad[0, c], size=k, mode="nearest")
+        hi = maximum_filter(rad[0, c], size=k, mode="nearest")
+        assert np.all(out[c] >= lo * (1 - 1e-15)) and np.all(out[c] <= hi * (1 + 1e-15))
+
+
+def test_linear_in_radiance_and_shift_invariant_in_importance(oracle_mod):
+    H, W = 10, 12
+    r1, imp, blend = _rand_inputs(H, W, 2, RNG)
+    r2, _, _ = _rand_inputs(H, W, 2, RNG)
+    sizes = [3, 5]
+    o1 = oracle_mod.decode_filter_fuse(r1, imp, blend, sizes)
+    o2 = oracle_mod.decode_filter_fuse(r2, imp, blend, sizes)
+    a, b = np.float32(0.75), np.float32(2.0)
+    o12 = oracle_mod.decode_filter_fuse(a * r1 + b * r2, imp, blend, sizes)
+    # a*r1 + b*r2 is rounded to fp32 once; compare with that tolerance
+    np.testing.assert_allclose(o12, 0.75 * o1 + 2.0 * o2, rtol=2e-7)
+    # I -> I + const ("a relative value")
+    o_shift = oracle_mod.decode_filter_fuse(r1, imp + np.float32(7.0), blend, sizes)
+    np.testing.assert_allclose(o_shift, o1, rtol=2e-6)  # I+7 rounds I in fp32
+    # logits -> logits + const
+    o_lshift = oracle_mod.decode_filter_fuse(r1, imp, blend + np.float32(3.0), sizes)
+    np.testing.assert_allclose(o_lshift, o1, rtol=2e-6)
+
+
+@pytest.mark.parametrize("op", ["flipud", "fliplr", "transpose"])
+def test_flip_transpose_equivariance_everywhere(oracle_mod, op):
+    # The clamp border is symmetric, so the whole map (borders included) is
+    # equivariant under the dihedral symmetries of the grid.
+    H, W = 11, 16
+    rad, imp, blend = _rand_inputs(H, W, 3, RNG)
+    sizes = [3, 5, 9]
+    f = {"flipud": lambda a: a[..., ::-1, :], "fliplr": lambda a: a[..., ::-1],
+         "transpose": lambda a: np.swapaxes(a, -1, -2)}[op]
+    o = oracle_mod.decode_filter_fuse(rad, imp, blend, sizes)
+    of = oracle_mod.decode_filter_fuse(f(rad), f(imp), f(blend), sizes)
+    np.testing.assert_allclose(of, f(o), rtol=1e-13)
+
+
+def test_interior_translation_equivariance(oracle_mod):
+    H, W, k, s = 24, 24, 5, 3
+    rad, imp, _ = _rand_inputs(H, W, 1, RNG)
+    o = oracle_mod.decode_filter_fuse(rad, imp, None, [k])[0]
+    o_s = oracle_mod.decode_filter_fuse(np.roll(rad, (s, s), (-2, -1)),
+                                        np.roll(imp, (s, s), (-2, -1)), None, [k])[0]
+    r = k // 2
+    inner = np.s_[:, r + s:H - r, r + s:W - r]
+    np.testing.assert_allclose(o_s[inner], np.roll(o, (s, s), (-2, -1))[inner], rtol=1e-13)
+
+
+# ------------------------------------------------------------------ fusion (Eq. 5)
+def _filtered(oracle_mod, rad, imp, sizes):
+    return np.stack([oracle_mod.decode_filter_fuse(rad, imp[:, i:i + 1], None, [k])[0]
+                     for i, k in enumerate(sizes)])
+
+
+def test_fusion_equal_logits_is_mean_and_dominant_logit_selects(oracle_mod):
+    H, W = 13, 14
+    sizes = [3, 7, 11]
+    rad, imp, _ = _rand_inputs(H, W, 3, RNG)
+    Ri = _filtered(oracle_mod, rad, imp, sizes)
+    eq = np.zeros((1, 3, H, W), np.float32)
+    out = oracle_mod.decode_filter_fuse(rad, imp, eq, sizes)[0]
+    np.testing.assert_allclose(out, Ri.mean(0), rtol=1e-14)
+    # a dominant logit on map 1 selects R^{k_1} (catches alpha_i paired with R_j)
+    dom = np.zeros((1, 3, H, W), np.float32)
+    dom[:, 1] = 40.0
+    out = oracle_mod.decode_filter_fuse(rad, imp, dom, sizes)[0]
+    np.testing.assert_allclose(out, Ri[1], rtol=1e-8)
+    # and R^{k_1} itself is the closed-form ratio of box filters for k=7
+    e = np.exp(imp[0, 1].astype(np.float64))
+    ref = _box(e * rad[0, 0], 7) / _box(e, 7)
+    np.testing.assert_allclose(Ri[1][0], ref, rtol=1e-12)
+
+
+def test_fusion_M1_identity_and_prenormalised_alpha(oracle_mod):
+    H, W = 8, 9
+    rad, imp, _ = _rand_inputs(H, W, 2, RNG)
+    one = oracle_mod.decode_filter_fuse(rad, imp[:, :1], None, [5])
+    with_logit = oracle_mod.decode_filter_fuse(rad, imp[:, :1],
+                                               np.full((1, 1, H, W), 3.0, np.float32), [5])
+    assert np.array_equal(one, with_logit)
+    Ri = _filtered(oracle_mod, rad, imp, [3, 5])
+    a = RNG.uniform(0, 1, (1, 1, H, W)).astype(np.float32)
+    alpha = np.concatenate([a, 1 - a], axis=1).astype(np.float32)
+    out = oracle_mod.decode_filter_fuse(rad, imp, alpha, [3, 5], blend_is_logits=False)[0]
+    ref = alpha[0, 0].astype(np.float64) * Ri[0] + alpha[0, 1].astype(np.float64) * Ri[1]
+    np.testing.assert_allclose(out, ref, rtol=1e-14)
+
+
+def test_fuse_entry_point_closed_form(oracle_mod):
+    H, W, M = 4, 5, 3
+    filt = RNG.standard_normal((M, 3, H, W))
+    logits = RNG.standard_normal((M, H, W)).astype(np.float32)
+    out = oracle_mod.fuse(filt, logits)
+    a = np.exp(logits.astype(np.float64))
+    a /= a.sum(0)
+    np.testing.assert_allclose(out, (a[:, None] * filt).sum(0), rtol=1e-14)
+
+
+# --------------------------------------------------------- hand-worked golden
+def test_hand_worked_3x3_golden(oracle_mod):
+    g = json.load(open(os.path.join(HERE, "golden", "hand_worked_3x3.json")))
+    H, W = g["H"], g["W"]
+    imp = np.stack([np.log(np.array(g["exp_importance_k1"], np.float64)),
+                    np.log(np.array(g["exp_importance_k3"], np.float64))]).astype(np.float32)
+    red = np.array(g["radiance_R"], np.float32)
+    rad = np.stack([red, np.ones((H, W), np.float32), 10 - red])[None]
+    blend = np.stack([np.full((H, W), np.log(float(v)), np.float32) for v in g["exp_blend"]])[None]
+    out = oracle_mod.decode_filter_fuse(rad, imp[None], blend, g["sizes"])[0]
+    k3 = oracle_mod.decode_filter_fuse(rad, imp[None, 1:2], None, [3])[0]
+    # the inputs are fp32 roundings of ln(n); the tolerance covers that (~1e-7)
+    for key, frac in g["expected_k3_R"].items():
+        y, x = eval(key)
+        assert k3[0, y, x] == pytest.approx(float(Fraction(frac)), rel=2e-7)
+    for key, frac in g["expected_fused_R"].items():
+        y, x = eval(key)
+        assert out[0, y, x] == pytest.approx(float(Fraction(frac)), rel=2e-7)
+        assert out[2, y, x] == pytest.approx(10 - float(Fraction(frac)), rel=2e-7)
+    np.testing.assert_allclose(out[1], 1.0, rtol=1e-15)
+
+
+# ------------------------------------------------------- 50-digit brute force
+def _brute(rad, imp, blend, sizes):
+    """Eq. 3-5 per (p, q) pair at 50 digits, no max shift, no shared helpers."""
+    mpmath.mp.dps = 50
+    _, H, W = rad.shape
+    M = len(sizes)
+    out = np.zeros((3, H, W))
+    for y in range(H):
+        for x in range(W):
+            Rs = []
+            for i, k in enumerate(sizes):
+                r = k // 2
+                taps = [(min(max(y + dy, 0), H - 1), min(max(x + dx, 0), W - 1))
+                        for dy in range(-r, r + 1) for dx in range(-r, r + 1)]
+                den = mpmath.fsum(mpmath.exp(mpmath.mpf(float(imp[i, qy, qx])))
+                                  for qy, qx in taps)
+                Rs.append([mpmath.fsum(mpmath.exp(mpmath.mpf(float(imp[i, qy, qx])))
+                                       * mpmath.mpf(float(rad[c, qy, qx]))
+                                       for qy, qx in taps) / den for c in range(3)])
+            if M == 1:
+                alpha = [mpmath.mpf(1)]
+            else:
+                a = [mpmath.exp(mpmath.mpf(float(blend[i, y, x]))) for i in range(M)]
+                s = mpmath.fsum(a)
+                alpha = [ai / s for ai in a]
+            for c in range(3):
+                out[c, y, x] = float(mpmath.fsum(alpha[i] * Rs[i][c] for i in range(M)))
+    return out
+
+
+@pytest.mark.parametrize("sizes", [[3], [5, 3], [1, 3, 7], [7, 5, 3]])
+def test_brute_force_8x8_mpmath(oracle_mod, sizes):
+    rng = np.random.default_rng(len(sizes) * 31 + sizes[0])
+    H = W = 8
+    rad, imp, blend = _rand_inputs(H, W, len(sizes), rng, imp_scale=3.0)
+    out = oracle_mod.decode_filter_fuse(rad, imp, blend if len(sizes) > 1 else None, sizes)[0]
+    ref = _brute(rad[0], imp[0], blend[0], sizes)
+    np.testing.assert_allclose(out, ref, rtol=1e-13, atol=0)
+
+
+# --------------------------------------------- internal consistency + API edges
+def test_streaming_equals_explicit_and_rows_pixels_agree(oracle_mod):
+    H, W = 21, 18
+    sizes = [3, 5, 7, 9, 11, 13]
+    rad, imp, blend = _rand_inputs(H, W, 6, RNG)
+    s = oracle_mod.decode_filter_fuse(rad, imp, blend, sizes)
+    e = oracle_mod.explicit_decode_filter_fuse(rad[0], imp[0], blend[0], sizes)
+    np.testing.assert_allclose(s[0], e, rtol=1e-14)
+    rows = oracle_mod.decode_filter_fuse(rad, imp, blend, sizes, rows=(5, 12))
+    assert np.array_equal(rows, s[:, :, 5:12])
+    ys, xs = np.array([0, 20, 7]), np.array([17, 0, 9])
+    px = oracle_mod.decode_filter_fuse_pixels(rad, imp, blend, sizes, [0, 0, 0], ys, xs)
+    assert np.array_equal(px, s[0][:, ys, xs].T)
+
+
+def test_oracle_rejects_bad_config(oracle_mod):
+    rad, imp, blend = _rand_inputs(6, 6, 2, RNG)
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 4])      # even k
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 7])      # k > min(H,W)
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.decode_filter_fuse(rad, imp, None, [3, 5])       # M > 1 needs blend
+
+
+def test_softmax_stays_finite_for_huge_importance(oracle_mod):
+    # DESIGN.md R2: the max-shifted softmax equals Eq. 3 exactly and stays
+    # finite where exp(I) itself would overflow (exp(1000) = inf in fp64).
+    imap = np.full((5, 5), -1000.0, np.float32)
+    imap[4, 4] = 1000.0       # the last tap (j = 8) of pixel (3,3)'s window
+    km = oracle_mod.kernel_map(imap, 3)
+    assert np.all(np.isfinite(km))
+    np.testing.assert_allclose(km.sum(-1), 1.0, rtol=0, atol=1e-15)
+    assert km[3, 3, 8] == 1.0 and km[0, 0, 0] == pytest.approx(1 / 9, rel=1e-15)
