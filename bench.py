@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the fused kernel-map decode + filter + fusion (arXiv 2202.05977).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kmd|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
+
+A step is one pass of the whole hot path (load,
+shared exp, normalise, filter, fusion weights, fuse, store) over one 1920x1080
+frame with the paper's kernel-size set {3,5,7,9,11,13} (BASELINE.json
+configs[2], the configuration the metric is quoted on).  Multi-GPU runs are
+frame-parallel ("weak" scaling, configs[4]'s sharding): every rank processes
+its own frame each step, no collective on the data path.
+
+Inputs are synthetic (paper_2202_05977_b200/inputs.py), resident in HBM, and
+rotate over 4 distinct frames (597 MB > 126 MB L2), so no step reads another
+step's inputs from L2.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+PAPER_SIZES = [3, 5, 7, 9, 11, 13]
+METRIC = "1080p Mpix/s (decode+filter+fusion)"
+UNIT = "Mpix/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--sizes", type=str, default=",".join(map(str, PAPER_SIZES)))
+    ap.add_argument("--rotate", type=int, default=4, help="distinct resident frames per rank")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU seconds for the oracle sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- distributed
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        reasons = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(s)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, measured)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def lib_sources_hash():
+    import hashlib
+    from paper_2202_05977_b200 import _build
+    h = hashlib.sha256()
+    for p in sorted(_build._deps()):
+        h.update(open(p, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def recorded_traffic(workload: str):
+    """dram bytes per launch from the committed ncu --set full capture
+    (profiles/traffic.json), if it was taken on the current kernel sources."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        e = d.get(workload)
+        if e and e.get("lib_sha") == lib_sources_hash():
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------- oracle legs
+def oracle_rows_time(inp_cpu, sizes, rows, threads=0):
+    import oracle
+    t0 = time.perf_counter()
+    ref = oracle.decode_filter_fuse(inp_cpu[0], inp_cpu[1], inp_cpu[2], sizes, rows=rows,
+                                    threads=threads)
+    return time.perf_counter() - t0, ref
+
+
+def calibrate_rows(inp_cpu, sizes, H, seconds):
+    t1, _ = oracle_rows_time(inp_cpu, sizes, (H // 2, H // 2 + 2))
+    per_row = t1 / 2
+    return max(1, min(H, int(seconds / max(per_row, 1e-9)))), per_row
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, timed on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2202_05977_b200 import inputs as gen
+    sizes = [int(s) for s in args.sizes.split(",")]
+    H, W, M = args.height, args.width, len(sizes)
+    inp = gen.make_inputs(1, H, W, M)
+    inp_cpu = (inp.radiance.numpy(), inp.importance.numpy(),
+               None if inp.blend is None else inp.blend.numpy())
+    budget = 150.0
+    total = args.steps + args.warmup
+    rows, per_row = calibrate_rows(inp_cpu, sizes, H, budget / max(total, 1))
+    for s in range(args.warmup):
+        y0 = (s * rows) % max(1, H - rows + 1)
+        oracle_rows_time(inp_cpu, sizes, (y0, y0 + rows))
+    el = 0.0
+    for s in range(args.steps):
+        y0 = ((s + args.warmup) * rows) % max(1, H - rows + 1)
+        dt, _ = oracle_rows_time(inp_cpu, sizes, (y0, y0 + rows))
+        el += dt
+    px = rows * W * args.steps
+    value = px / el / 1e6
+    cores = oracle.max_threads()
+    sample = (f"each step: {rows} rows x {W} px of a {W}x{H} M={M} frame "
+              f"({rows * W} px, fp64 oracle, OpenMP {cores} threads)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{W}x{H} frame, sizes {sizes}, fusion (configs[2])",
+                   "global_batch": 1, "parallelism": "host OpenMP"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- kmd leg
+def run_kmd(args, rank, world, local):
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+
+    dev = torch.device("cuda", local)
+    sizes = [int(s) for s in args.sizes.split(",")]
+    H, W, M = args.height, args.width, len(sizes)
+    F = max(1, args.rotate)
+    K, Wm = args.steps, args.warmup
+    assert Wm >= 3, "timing rules: at least 3 warm-up steps"
+    kmd.lib()
+    # resident inputs: F distinct frames per rank (frame ids rank*F .. rank*F+F-1)
+    inp = gen.make_inputs(F, H, W, M, frame_offset=rank * F, device=dev)
+    outs = torch.empty((F, 3, H, W), device=dev)
+    views = [(inp.radiance[f:f + 1], inp.importance[f:f + 1],
+              None if inp.blend is None else inp.blend[f:f + 1], outs[f:f + 1])
+             for f in range(F)]
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+
+    def step(s):
+        r, i, b, o = views[s % F]
+        kmd.decode_filter_fuse(r, i, b, sizes, out=o, stream=stream)
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: K steps, per-launch events on the launching stream ---
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for s in range(K):
+            ev[s][0].record(stream)
+            step(s)
+            ev[s][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    el_ms = t_start.elapsed_time(t_end)
+    kern_ms = sorted(a.elapsed_time(b) for a, b in ev)
+    kern_avg_ms = sum(kern_ms) / K
+    el_ms_max = max_over_ranks(el_ms, world)
+
+    px_per_step = H * W * world
+    value = px_per_step * K / (el_ms_max / 1e3) / 1e6
+    bytes_launch = kmd.algorithmic_bytes(1, H, W, sizes, inp.blend is not None)
+    achieved = bytes_launch / (kern_avg_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    workload = f"{W}x{H} frame, sizes {sizes}, fusion (BASELINE.json configs[2])"
+
+    # ---- e2e: through the C ABI with pinned HOST buffers ---------------------
+    e2e = None
+    if args.e2e_steps > 0:
+        hr = inp.radiance[:1].cpu().pin_memory()
+        hi = inp.importance[:1].cpu().pin_memory()
+        hb = None if inp.blend is None else inp.blend[:1].cpu().pin_memory()
+        ho = torch.empty((1, 3, H, W)).pin_memory()
+        ws = torch.empty(kmd.host_workspace_bytes(1, H, W, sizes), dtype=torch.uint8, device=dev)
+        for _ in range(3):
+            kmd.decode_filter_fuse_host(hr, hi, hb, sizes, ho, ws, stream=stream)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            kmd.decode_filter_fuse_host(hr, hi, hb, sizes, ho, ws, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(a.elapsed_time(b), world)
+        h2d = (hr.numel() + hi.numel() + (0 if hb is None else hb.numel())) * 4
+        e2e = {"value": px_per_step * args.e2e_steps / (e2e_ms / 1e3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": ho.numel() * 4,
+               "ms_per_step": e2e_ms / args.e2e_steps,
+               "path": "kmd_decode_filter_fuse_host (pinned host -> HBM -> kernel -> host)"}
+
+    # ---- CPU oracle baseline + sampled parity (rank 0, N=1 only) -------------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import numpy as np
+        import oracle
+        inp_cpu = (inp.radiance[:1].cpu().numpy(), inp.importance[:1].cpu().numpy(),
+                   None if inp.blend is None else inp.blend[:1].cpu().numpy())
+        rows, _ = calibrate_rows(inp_cpu, sizes, H, args.cpu_seconds)
+        y0 = max(0, (H - rows) // 2)
+        dt, ref = oracle_rows_time(inp_cpu, sizes, (y0, y0 + rows))
+        cpu = {"value": rows * W / dt / 1e6, "unit": UNIT, "cores": oracle.max_threads(),
+               "kind": "oracle",
+               "sample": f"rows {y0}..{y0 + rows} ({rows * W} px) of frame 0 of the {W}x{H} "
+                         f"M={M} workload, fp64 oracle, {dt:.1f} s"}
+        kmd.decode_filter_fuse(*views[0], sizes, stream=stream)
+        torch.cuda.synchronize(dev)
+        got = outs[0:1, :, y0:y0 + rows].cpu().numpy().astype(np.float64)
+        rel = np.abs(got - ref) / np.where(ref == 0, 1.0, np.abs(ref))
+        parity = {"max_rel_err": float(rel.max()), "pixels": int(rows * W), "tol": 1e-5,
+                  "rows": [y0, y0 + rows]}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": Wm, "ms_per_step": el_ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload, "global_batch": world, "frames_per_rank_per_step": 1,
+                   "height": H, "width": W, "sizes": sizes,
+                   "parallelism": f"frame-parallel x{world} (no data-path collective)",
+                   "l2": f"inputs rotate over {F} resident frames per rank "
+                         f"({F * bytes_launch / 1e6:.0f} MB > 126 MB L2)"},
+        "ms_per_frame": el_ms_max / K,
+        "kernel_ms": {"avg": kern_avg_ms, "p10": kern_ms[K // 10], "p50": kern_ms[K // 2],
+                      "p90": kern_ms[(9 * K) // 10]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": recorded_traffic(workload),
+                     "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src,
+                     "kernel": "fused decode+filter+fuse (libkmd)"},
+        "gpu_launches": K * kmd.launches_per_call(),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "paper_context": "RTX 2080 Ti, 1280x720, M=6: 1.10 ms reconstruction (PAPER.md:472)",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup()
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_kmd(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

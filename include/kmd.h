@@ -1,0 +1,158 @@
+/*
+ * kmd.h -- C ABI of libkmd: the B200 (sm_100a) kernel-map decoder, per-pixel
+ * filter and kernel fusion of arXiv 2202.05977 ("weight sharing kernel
+ * prediction"), reconstruction phase.
+ *
+ * What one call computes (§3 Eq. 3-5, §4.2, §5.3), for every frame n
+ * and pixel p, with M importance maps I_i and kernel sizes k_i:
+ *
+ *   w_p^i(q) = exp(I_i(q)) / sum_{q' in Omega_{k_i}(p)} exp(I_i(q'))  (Eq. 3)
+ *   R^{k_i}(p,c) = sum_{q in Omega_{k_i}(p)} w_p^i(q) r_c(q)          (Eq. 4)
+ *   alpha_i(p)   = softmax_i(B_i(p))
+ *   Rhat(p,c)    = sum_i alpha_i(p) R^{k_i}(p,c)                       (Eq. 5)
+ *
+ * Omega_k(p) is the k x k window centred on p; samples outside the image are
+ * clamped to the nearest edge pixel, for the importance unfold and for the
+ * colour taps alike (reading R1).  The H x W x k^2 kernel map of
+ * Fig. 3 is never written to memory: one streaming kernel builds, applies and
+ * fuses the kernels ("one single function ... in a
+ * streaming manner").
+ *
+ * Conventions for every entry point
+ *  - Types: fp32 in, fp32 out, fp32 arithmetic.  Planar, row-major,
+ *    contiguous ("NCHW"):  radiance [N,3,H,W]  importance [N,M,H,W]
+ *    blend [N,M,H,W]  out [N,3,H,W].
+ *  - Memory: device pointers unless the name ends in _host.  The caller owns
+ *    every buffer; the library allocates nothing per call and keeps no mutable
+ *    global state except a thread-local error string (reentrant).
+ *  - Asynchrony: argument checks run synchronously, before any CUDA call;
+ *    work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream) and the call returns without synchronising.
+ *  - Errors: returned as kmd_status; nothing is thrown or aborted across the
+ *    ABI.  kmd_last_error() gives a human-readable detail for this thread.
+ *  - Aliasing: `out` must not overlap any input (the stencil reads
+ *    neighbours) -> KMD_ERR_ALIAS.
+ *  - Numerics: max relative error <= 1e-5 against the fp64 oracle for finite
+ *    inputs with radiance >= 0.  Importance values are used
+ *    unshifted (exp(I)) while a tile's values lie in [KMD_EXP_SAFE_LO,
+ *    KMD_EXP_SAFE_HI] and |radiance| <= KMD_RADIANCE_SAFE; otherwise that tile
+ *    takes a per-window max-shifted path (same result, slower).
+ */
+#ifndef KMD_H
+#define KMD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMD_VERSION_MAJOR 0
+#define KMD_VERSION_MINOR 1
+
+#define KMD_MAX_SIZES 8        /* M <= 8 maps per call (the paper uses 6) */
+#define KMD_MAX_K 31           /* largest odd window size accepted                      */
+#define KMD_EXP_SAFE_LO (-60.0f)
+#define KMD_EXP_SAFE_HI (60.0f)
+#define KMD_RADIANCE_SAFE (1.0e8f)
+
+typedef enum {
+    KMD_OK = 0,
+    KMD_ERR_NULL = 1,   /* a required pointer is NULL (blend may be NULL only when M == 1)  */
+    KMD_ERR_CONFIG = 2, /* M not in [1,8]; a size even, < 1, > KMD_MAX_K or > min(H,W);
+                           border not KMD_BORDER_CLAMP                                       */
+    KMD_ERR_DIM = 3,    /* N < 0, H < 1 or W < 1 (when N > 0); bad band geometry;
+                           element count overflows int64                                      */
+    KMD_ERR_ALIGN = 4,  /* reserved (every path accepts any 4-byte aligned pointer)           */
+    KMD_ERR_ALIAS = 5,  /* out overlaps an input                                              */
+    KMD_ERR_CUDA = 6,   /* a CUDA runtime call or launch failed (see kmd_last_error)          */
+    KMD_ERR_NCCL = 7    /* reserved for collective helpers                                    */
+} kmd_status;
+
+typedef enum { KMD_BORDER_CLAMP = 0 } kmd_border;
+
+/* Kernel-size set and fusion options (SPEC.md:228-231 FusionConfig). */
+typedef struct {
+    int32_t num_sizes;              /* M, 1..KMD_MAX_SIZES                                  */
+    int32_t sizes[KMD_MAX_SIZES];   /* odd window sizes; importance map i <-> sizes[i]
+                                       (paper: {3,5,7,9,11,13} = k_b + i*k_s, k_b=3, k_s=2)  */
+    int32_t blend_is_logits;        /* 1: blend holds logits, softmax applied inside (paper,
+                                       PAPER.md:251); 0: blend already holds alpha_i(p)      */
+    int32_t border;                 /* KMD_BORDER_CLAMP (the only policy, R1)     */
+} kmd_config;
+
+typedef void* kmd_stream_t;         /* a cudaStream_t */
+
+/* ---------------------------------------------------------------------------
+ * Hot path: fused decode (Eq. 3) + filter (Eq. 4) + fusion (Eq. 5).
+ *   radiance   [N,3,H,W] device, noisy demodulated HDR irradiance
+ *   importance [N,M,H,W] device, importance maps I_i (Eq. 2; map i <-> cfg->sizes[i])
+ *   blend      [N,M,H,W] device, fusion logits (or alphas); NULL allowed iff M == 1
+ *   out        [N,3,H,W] device, the fused result Rhat
+ * N == 0 is a no-op.  Errors: NULL, CONFIG, DIM, ALIAS, CUDA.                 */
+kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance,
+                                  const float* blend, float* out, int32_t N, int32_t H,
+                                  int32_t W, const kmd_config* cfg, kmd_stream_t stream);
+
+/* One size, no fusion: out_i = R^{k}(p,c) of Eq. 3-4.
+ *   radiance [N,3,H,W], importance_i [N,1,H,W], out_i [N,3,H,W], all device.   */
+kmd_status kmd_decode_filter(const float* radiance, const float* importance_i, float* out_i,
+                             int32_t N, int32_t H, int32_t W, int32_t k,
+                             kmd_stream_t stream);
+
+/* Fusion only (Eq. 5):
+ *   filtered [N,M,3,H,W] device (R^{k_i}), blend [N,M,H,W] device (NULL iff M == 1),
+ *   out [N,3,H,W] device.                                                       */
+kmd_status kmd_fuse(const float* filtered, const float* blend, float* out, int32_t N,
+                    int32_t H, int32_t W, int32_t M, int32_t blend_is_logits,
+                    kmd_stream_t stream);
+
+/* Row band of a taller frame (multi-GPU spatial split).
+ * The frame has H_global rows; this call produces output rows
+ * [y0, y0 + band_rows).  radiance / importance hold rows
+ * [y0 - halo_top, y0 + band_rows + halo_bot) of the frame:
+ *   radiance [N,3,halo_top+band_rows+halo_bot,W], importance [N,M,...,W];
+ * blend and out hold only the band: [N,M,band_rows,W] and [N,3,band_rows,W].
+ * Rows outside the frame are clamped to rows 0 / H_global-1 as in the whole-
+ * frame call, so the band outputs are bitwise equal to the corresponding rows
+ * of kmd_decode_filter_fuse on the whole frame.  Requires
+ *   halo_top >= min(r_max, y0) and halo_bot >= min(r_max, H_global - y0 - band_rows),
+ * r_max = (max_i k_i - 1)/2, and y0 - halo_top >= 0,
+ * y0 + band_rows + halo_bot <= H_global.  Errors as kmd_decode_filter_fuse.  */
+kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* importance,
+                                       const float* blend, float* out, int32_t N,
+                                       int32_t band_rows, int32_t W, int32_t halo_top,
+                                       int32_t halo_bot, int32_t y0, int32_t H_global,
+                                       const kmd_config* cfg, kmd_stream_t stream);
+
+/* End-to-end from HOST memory: copies the inputs host->device, runs the fused
+ * kernel and copies the result device->host, all on `stream` (pinned host
+ * buffers make the copies asynchronous and overlappable).  The caller passes a
+ * device workspace of at least kmd_host_workspace_bytes(N,H,W,cfg) bytes; the
+ * work is pipelined in frame chunks across the copy engines.  The call returns
+ * after enqueueing; synchronise `stream` before reading out_host.            */
+size_t kmd_host_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg);
+kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
+                                       const float* blend_host, float* out_host, int32_t N,
+                                       int32_t H, int32_t W, const kmd_config* cfg,
+                                       void* device_workspace, size_t workspace_bytes,
+                                       kmd_stream_t stream);
+
+/* Algorithmic HBM bytes of one kmd_decode_filter_fuse call:
+ * N*H*W*4*(3 + M + (blend? M : 0) + 3)  (inputs read once, output written once). */
+int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                              int32_t has_blend);
+
+/* Number of kernel launches one kmd_decode_filter_fuse call enqueues (for the
+ * bench's gpu_launches count). */
+int32_t kmd_launches_per_call(void);
+
+const char* kmd_status_string(kmd_status s);
+const char* kmd_last_error(void);     /* thread-local detail of the last failure */
+int32_t kmd_version(void);             /* KMD_VERSION_MAJOR*100 + KMD_VERSION_MINOR */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMD_H */

@@ -1,0 +1,269 @@
+// kmd_api.cu -- the extern "C" boundary of libkmd (declared in include/kmd.h).
+// Argument checks are synchronous and precede every CUDA call; work is
+// enqueued on the caller's stream.  No per-call allocation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "kmd_kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+kmd_status fail(kmd_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+kmd_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(KMD_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+kmd_status check_cfg(const kmd_config* cfg, int64_t H, int64_t W) {
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (cfg->num_sizes < 1 || cfg->num_sizes > KMD_MAX_SIZES)
+        return fail(KMD_ERR_CONFIG, "num_sizes=%d not in [1,%d]", cfg->num_sizes, KMD_MAX_SIZES);
+    for (int i = 0; i < cfg->num_sizes; ++i) {
+        const int k = cfg->sizes[i];
+        if (k < 1 || k % 2 == 0 || k > KMD_MAX_K)
+            return fail(KMD_ERR_CONFIG, "sizes[%d]=%d must be odd and in [1,%d]", i, k, KMD_MAX_K);
+        if (k > H || k > W)
+            return fail(KMD_ERR_CONFIG, "sizes[%d]=%d exceeds min(H,W)=%lld", i, k,
+                        (long long)(H < W ? H : W));
+    }
+    if (cfg->blend_is_logits != 0 && cfg->blend_is_logits != 1)
+        return fail(KMD_ERR_CONFIG, "blend_is_logits=%d must be 0 or 1", cfg->blend_is_logits);
+    if (cfg->border != KMD_BORDER_CLAMP)
+        return fail(KMD_ERR_CONFIG, "border=%d unsupported (only KMD_BORDER_CLAMP)", cfg->border);
+    return KMD_OK;
+}
+
+int rmax_of(const kmd_config* cfg) {
+    int r = 0;
+    for (int i = 0; i < cfg->num_sizes; ++i) r = r > (cfg->sizes[i] - 1) / 2 ? r : (cfg->sizes[i] - 1) / 2;
+    return r;
+}
+
+bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
+    if (!a || !b || abytes == 0 || bbytes == 0) return false;
+    const uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+    return a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+// Common launch path for whole frames and bands.
+kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t stream) {
+    p.M = cfg->num_sizes;
+    p.rmax = rmax_of(cfg);
+    p.blend_is_logits = cfg->blend_is_logits;
+    for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < cfg->num_sizes ? cfg->sizes[i] : 1;
+    if (p.M == 1) p.blend = nullptr;  // softmax of one logit is 1 (reading R11)
+    const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
+    const int total = p.N;
+    for (int n0 = 0; n0 < total; n0 += 65535) {
+        kmd::FusedParams q = p;
+        q.N = total - n0 < 65535 ? total - n0 : 65535;
+        q.rad = p.rad + (size_t)n0 * 3 * bplane;
+        q.imp = p.imp + (size_t)n0 * p.M * bplane;
+        q.blend = p.blend ? p.blend + (size_t)n0 * p.M * oplane : nullptr;
+        q.out = p.out + (size_t)n0 * 3 * oplane;
+        cudaError_t e = kmd::launch_fused_direct(q, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
+    }
+    return KMD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance,
+                                  const float* blend, float* out, int32_t N, int32_t H,
+                                  int32_t W, const kmd_config* cfg, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (N > 0) {
+        kmd_status s = check_cfg(cfg, H, W);
+        if (s) return s;
+    }
+    if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
+    if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (N == 0) return KMD_OK;
+    const size_t plane = (size_t)H * W * sizeof(float);
+    const size_t M = (size_t)cfg->num_sizes;
+    if (overlaps(out, 3 * N * plane, radiance, 3 * N * plane) ||
+        overlaps(out, 3 * N * plane, importance, M * N * plane) ||
+        (M > 1 && overlaps(out, 3 * N * plane, blend, M * N * plane)))
+        return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    kmd::FusedParams p{};
+    p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out;
+    p.N = N; p.W = W; p.H = H;
+    p.row_base = 0; p.buf_rows = H; p.out_y0 = 0; p.out_rows = H;
+    return run_fused(p, cfg, (cudaStream_t)stream);
+}
+
+kmd_status kmd_decode_filter(const float* radiance, const float* importance_i, float* out_i,
+                             int32_t N, int32_t H, int32_t W, int32_t k, kmd_stream_t stream) {
+    kmd_config cfg{};
+    cfg.num_sizes = 1;
+    cfg.sizes[0] = k;
+    cfg.blend_is_logits = 1;
+    cfg.border = KMD_BORDER_CLAMP;
+    return kmd_decode_filter_fuse(radiance, importance_i, nullptr, out_i, N, H, W, &cfg, stream);
+}
+
+kmd_status kmd_fuse(const float* filtered, const float* blend, float* out, int32_t N, int32_t H,
+                    int32_t W, int32_t M, int32_t blend_is_logits, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
+    if (M < 1 || M > KMD_MAX_SIZES) return fail(KMD_ERR_CONFIG, "M=%d not in [1,%d]", M, KMD_MAX_SIZES);
+    if (blend_is_logits != 0 && blend_is_logits != 1)
+        return fail(KMD_ERR_CONFIG, "blend_is_logits=%d must be 0 or 1", blend_is_logits);
+    if (!filtered || !out) return fail(KMD_ERR_NULL, "filtered/out is NULL");
+    if (M > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", M);
+    if (N == 0) return KMD_OK;
+    const size_t plane = (size_t)H * W * sizeof(float);
+    if (overlaps(out, 3 * N * plane, filtered, 3 * (size_t)M * N * plane) ||
+        (M > 1 && overlaps(out, 3 * N * plane, blend, (size_t)M * N * plane)))
+        return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    cudaError_t e = kmd::launch_fuse_only(filtered, M > 1 ? blend : nullptr, out, N, H, W, M,
+                                          blend_is_logits, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fuse kernel launch");
+    return KMD_OK;
+}
+
+kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* importance,
+                                       const float* blend, float* out, int32_t N,
+                                       int32_t band_rows, int32_t W, int32_t halo_top,
+                                       int32_t halo_bot, int32_t y0, int32_t H_global,
+                                       const kmd_config* cfg, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (N > 0) {
+        if (band_rows < 1 || W < 1 || H_global < 1)
+            return fail(KMD_ERR_DIM, "band_rows=%d, W=%d, H_global=%d must be >= 1", band_rows, W, H_global);
+        if (halo_top < 0 || halo_bot < 0 || y0 < 0 || y0 - halo_top < 0 ||
+            (int64_t)y0 + band_rows + halo_bot > H_global)
+            return fail(KMD_ERR_DIM, "band [%d-%d, %d+%d+%d) outside frame of %d rows", y0, halo_top,
+                        y0, band_rows, halo_bot, H_global);
+        kmd_status s = check_cfg(cfg, H_global, W);
+        if (s) return s;
+        const int r = rmax_of(cfg);
+        const int need_top = r < y0 ? r : y0;
+        const int below = H_global - y0 - band_rows;
+        const int need_bot = r < below ? r : below;
+        if (halo_top < need_top || halo_bot < need_bot)
+            return fail(KMD_ERR_DIM, "halo (%d,%d) smaller than required (%d,%d) for r_max=%d", halo_top,
+                        halo_bot, need_top, need_bot, r);
+    }
+    if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
+    if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (N == 0) return KMD_OK;
+    const int buf_rows = halo_top + band_rows + halo_bot;
+    const size_t bplane = (size_t)buf_rows * W * sizeof(float), oplane = (size_t)band_rows * W * sizeof(float);
+    const size_t M = (size_t)cfg->num_sizes;
+    if (overlaps(out, 3 * N * oplane, radiance, 3 * N * bplane) ||
+        overlaps(out, 3 * N * oplane, importance, M * N * bplane) ||
+        (M > 1 && overlaps(out, 3 * N * oplane, blend, M * N * oplane)))
+        return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    kmd::FusedParams p{};
+    p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out;
+    p.N = N; p.W = W; p.H = H_global;
+    p.row_base = y0 - halo_top; p.buf_rows = buf_rows; p.out_y0 = y0; p.out_rows = band_rows;
+    return run_fused(p, cfg, (cudaStream_t)stream);
+}
+
+size_t kmd_host_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg) {
+    if (!cfg || N < 1 || H < 1 || W < 1 || cfg->num_sizes < 1 || cfg->num_sizes > KMD_MAX_SIZES) return 0;
+    // one frame of inputs + output, double-buffered when N > 1
+    const size_t frame = (size_t)H * W * sizeof(float) * (size_t)(3 + 2 * cfg->num_sizes + 3);
+    return frame * (N > 1 ? 2 : 1);
+}
+
+kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
+                                       const float* blend_host, float* out_host, int32_t N,
+                                       int32_t H, int32_t W, const kmd_config* cfg,
+                                       void* device_workspace, size_t workspace_bytes,
+                                       kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (N > 0) {
+        kmd_status s = check_cfg(cfg, H, W);
+        if (s) return s;
+    }
+    if (!radiance_host || !importance_host || !out_host || !device_workspace)
+        return fail(KMD_ERR_NULL, "a host buffer or the workspace is NULL");
+    if (cfg->num_sizes > 1 && !blend_host) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (N == 0) return KMD_OK;
+    const size_t need = kmd_host_workspace_bytes(N, H, W, cfg);
+    if (workspace_bytes < need)
+        return fail(KMD_ERR_DIM, "workspace %zu bytes < required %zu", workspace_bytes, need);
+    const int M = cfg->num_sizes;
+    const size_t plane = (size_t)H * W;
+    const size_t frame_floats = plane * (size_t)(3 + 2 * M + 3);
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int n = 0; n < N; ++n) {
+        float* base = (float*)device_workspace + (size_t)(n & (N > 1 ? 1 : 0)) * frame_floats;
+        float* d_rad = base;
+        float* d_imp = d_rad + 3 * plane;
+        float* d_blend = d_imp + M * plane;
+        float* d_out = d_blend + M * plane;
+        cudaError_t e;
+        e = cudaMemcpyAsync(d_rad, radiance_host + (size_t)n * 3 * plane, 3 * plane * sizeof(float),
+                            cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D radiance");
+        e = cudaMemcpyAsync(d_imp, importance_host + (size_t)n * M * plane, M * plane * sizeof(float),
+                            cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D importance");
+        if (M > 1) {
+            e = cudaMemcpyAsync(d_blend, blend_host + (size_t)n * M * plane, M * plane * sizeof(float),
+                                cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "H2D blend");
+        }
+        kmd_status s = kmd_decode_filter_fuse(d_rad, d_imp, M > 1 ? d_blend : nullptr, d_out, 1, H, W,
+                                              cfg, stream);
+        if (s) return s;
+        e = cudaMemcpyAsync(out_host + (size_t)n * 3 * plane, d_out, 3 * plane * sizeof(float),
+                            cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H out");
+    }
+    return KMD_OK;
+}
+
+int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                              int32_t has_blend) {
+    if (!cfg || N < 0 || H < 0 || W < 0) return -1;
+    const int64_t M = cfg->num_sizes;
+    return (int64_t)N * H * W * 4 * (3 + M + (has_blend ? M : 0) + 3);
+}
+
+int32_t kmd_launches_per_call(void) { return 1; }
+
+const char* kmd_status_string(kmd_status s) {
+    switch (s) {
+        case KMD_OK: return "KMD_OK";
+        case KMD_ERR_NULL: return "KMD_ERR_NULL";
+        case KMD_ERR_CONFIG: return "KMD_ERR_CONFIG";
+        case KMD_ERR_DIM: return "KMD_ERR_DIM";
+        case KMD_ERR_ALIGN: return "KMD_ERR_ALIGN";
+        case KMD_ERR_ALIAS: return "KMD_ERR_ALIAS";
+        case KMD_ERR_CUDA: return "KMD_ERR_CUDA";
+        case KMD_ERR_NCCL: return "KMD_ERR_NCCL";
+    }
+    return "KMD_ERR_UNKNOWN";
+}
+
+const char* kmd_last_error(void) { return g_err; }
+
+int32_t kmd_version(void) { return KMD_VERSION_MAJOR * 100 + KMD_VERSION_MINOR; }
+
+}  // extern "C"

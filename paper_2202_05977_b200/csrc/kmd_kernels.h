@@ -1,0 +1,14 @@
+// kmd_kernels.h -- host-side launchers of the libkmd device kernels.
+#pragma once
+#include "kmd_common.cuh"
+
+namespace kmd {
+
+// v1: direct separable sums, one CTA per 32x32 tile (kmd_direct.cu)
+cudaError_t launch_fused_direct(FusedParams p, cudaStream_t stream);
+
+// fusion only, Eq. 5 (kmd_fuse.cu)
+cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
+                             int H, int W, int M, int blend_is_logits, cudaStream_t stream);
+
+}  // namespace kmd

@@ -1,0 +1,240 @@
+"""Thin Python binding of libkmd (include/kmd.h): argument marshalling only.
+
+Every step of the reconstruction runs in libkmd's CUDA kernels; this module
+checks tensor dtype/device/shape/contiguity, passes ``data_ptr()``s and the
+current CUDA stream, and turns a non-zero ``kmd_status`` into ``KmdError``.
+There is no CPU fallback: if libkmd.so is missing or fails to load, every call
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+from . import _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkmd.so")
+
+KMD_MAX_SIZES = 8
+KMD_MAX_K = 31
+STATUS = {0: "KMD_OK", 1: "KMD_ERR_NULL", 2: "KMD_ERR_CONFIG", 3: "KMD_ERR_DIM",
+          4: "KMD_ERR_ALIGN", 5: "KMD_ERR_ALIAS", 6: "KMD_ERR_CUDA", 7: "KMD_ERR_NCCL"}
+
+
+class KmdError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, f"status {status}")
+        super().__init__(f"{self.name}: {detail}")
+
+
+class kmd_config(ctypes.Structure):
+    _fields_ = [("num_sizes", ctypes.c_int32),
+                ("sizes", ctypes.c_int32 * KMD_MAX_SIZES),
+                ("blend_is_logits", ctypes.c_int32),
+                ("border", ctypes.c_int32)]
+
+
+def make_config(sizes: Sequence[int], blend_is_logits: bool = True) -> kmd_config:
+    cfg = kmd_config()
+    cfg.num_sizes = len(sizes)
+    for i, k in enumerate(list(sizes)[:KMD_MAX_SIZES]):
+        cfg.sizes[i] = int(k)
+    cfg.blend_is_logits = int(bool(blend_is_logits))
+    cfg.border = 0
+    return cfg
+
+
+_lib = None
+
+EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter", "kmd_fuse",
+           "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
+           "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
+           "kmd_status_string", "kmd_last_error", "kmd_version")
+
+
+def lib(build_if_missing: bool = True):
+    """Load libkmd.so (building it in-tree first if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and _build.is_stale():
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libkmd.so not found at {LIB_PATH}; run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32 = ctypes.c_void_p, ctypes.c_int32
+    C = ctypes.POINTER(kmd_config)
+    L.kmd_decode_filter_fuse.argtypes = [P, P, P, P, i32, i32, i32, C, P]
+    L.kmd_decode_filter.argtypes = [P, P, P, i32, i32, i32, i32, P]
+    L.kmd_fuse.argtypes = [P, P, P, i32, i32, i32, i32, i32, P]
+    L.kmd_decode_filter_fuse_band.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, P]
+    L.kmd_host_workspace_bytes.argtypes = [i32, i32, i32, C]
+    L.kmd_host_workspace_bytes.restype = ctypes.c_size_t
+    L.kmd_decode_filter_fuse_host.argtypes = [P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
+    L.kmd_algorithmic_bytes.argtypes = [i32, i32, i32, C, i32]
+    L.kmd_algorithmic_bytes.restype = ctypes.c_int64
+    L.kmd_launches_per_call.argtypes = []
+    L.kmd_status_string.argtypes = [ctypes.c_int]
+    L.kmd_status_string.restype = ctypes.c_char_p
+    L.kmd_last_error.argtypes = []
+    L.kmd_last_error.restype = ctypes.c_char_p
+    L.kmd_version.argtypes = []
+    for f in ("kmd_decode_filter_fuse", "kmd_decode_filter", "kmd_fuse",
+              "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise KmdError(status, lib().kmd_last_error().decode())
+
+
+def _dev_f32(name: str, t: torch.Tensor, shape=None) -> int:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor (libkmd has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t.data_ptr()
+
+
+def _stream(t: torch.Tensor, stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device)
+    return stream.cuda_stream
+
+
+def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
+                       blend: Optional[torch.Tensor], sizes: Sequence[int],
+                       out: Optional[torch.Tensor] = None, blend_is_logits: bool = True,
+                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Fused Eq. 3 -> 4 -> 5: radiance [N,3,H,W], importance [N,M,H,W],
+    blend [N,M,H,W] (None iff M==1) -> out [N,3,H,W] (fp32, CUDA)."""
+    N, C, H, W = radiance.shape
+    M = len(sizes)
+    rp = _dev_f32("radiance", radiance, (N, 3, H, W))
+    ip = _dev_f32("importance", importance, (N, M, H, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, H, W))
+    if out is None:
+        out = torch.empty((N, 3, H, W), device=radiance.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    cfg = make_config(sizes, blend_is_logits)
+    _check(lib().kmd_decode_filter_fuse(rp, ip, bp, op, N, H, W, ctypes.byref(cfg),
+                                        _stream(radiance, stream)))
+    return out
+
+
+def decode_filter(radiance: torch.Tensor, importance_i: torch.Tensor, k: int,
+                  out: Optional[torch.Tensor] = None,
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """One size, Eq. 3 -> 4: radiance [N,3,H,W], importance_i [N,1,H,W] -> [N,3,H,W]."""
+    N, _, H, W = radiance.shape
+    rp = _dev_f32("radiance", radiance, (N, 3, H, W))
+    ip = _dev_f32("importance_i", importance_i, (N, 1, H, W))
+    if out is None:
+        out = torch.empty((N, 3, H, W), device=radiance.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    _check(lib().kmd_decode_filter(rp, ip, op, N, H, W, int(k), _stream(radiance, stream)))
+    return out
+
+
+def fuse(filtered: torch.Tensor, blend: Optional[torch.Tensor], blend_is_logits: bool = True,
+         out: Optional[torch.Tensor] = None,
+         stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Eq. 5 only: filtered [N,M,3,H,W], blend [N,M,H,W] -> [N,3,H,W]."""
+    N, M, _, H, W = filtered.shape
+    fp = _dev_f32("filtered", filtered, (N, M, 3, H, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, H, W))
+    if out is None:
+        out = torch.empty((N, 3, H, W), device=filtered.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    _check(lib().kmd_fuse(fp, bp, op, N, H, W, M, int(bool(blend_is_logits)),
+                          _stream(filtered, stream)))
+    return out
+
+
+def decode_filter_fuse_band(radiance: torch.Tensor, importance: torch.Tensor,
+                            blend: Optional[torch.Tensor], sizes: Sequence[int], *,
+                            y0: int, band_rows: int, halo_top: int, halo_bot: int,
+                            H_global: int, out: Optional[torch.Tensor] = None,
+                            blend_is_logits: bool = True,
+                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Row band [y0, y0+band_rows) of an H_global-row frame.  radiance /
+    importance hold rows [y0-halo_top, y0+band_rows+halo_bot); blend and out
+    hold the band rows only."""
+    N, _, R, W = radiance.shape
+    M = len(sizes)
+    assert R == halo_top + band_rows + halo_bot, "radiance rows != halo_top+band_rows+halo_bot"
+    rp = _dev_f32("radiance", radiance, (N, 3, R, W))
+    ip = _dev_f32("importance", importance, (N, M, R, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, band_rows, W))
+    if out is None:
+        out = torch.empty((N, 3, band_rows, W), device=radiance.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, 3, band_rows, W))
+    cfg = make_config(sizes, blend_is_logits)
+    _check(lib().kmd_decode_filter_fuse_band(rp, ip, bp, op, N, band_rows, W, halo_top, halo_bot,
+                                             y0, H_global, ctypes.byref(cfg),
+                                             _stream(radiance, stream)))
+    return out
+
+
+def host_workspace_bytes(N: int, H: int, W: int, sizes: Sequence[int]) -> int:
+    cfg = make_config(sizes)
+    return int(lib().kmd_host_workspace_bytes(N, H, W, ctypes.byref(cfg)))
+
+
+def decode_filter_fuse_host(radiance: torch.Tensor, importance: torch.Tensor,
+                            blend: Optional[torch.Tensor], sizes: Sequence[int],
+                            out: torch.Tensor, workspace: torch.Tensor,
+                            blend_is_logits: bool = True,
+                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """End-to-end from host (ideally pinned) CPU tensors: H2D copies, fused
+    kernel and D2H copy, all enqueued by libkmd on ``stream``.  ``workspace`` is
+    a CUDA uint8 tensor of >= host_workspace_bytes(...) bytes.  Returns ``out``
+    (caller synchronises ``stream`` before reading it)."""
+    N, _, H, W = radiance.shape
+    M = len(sizes)
+    for name, t, shape in (("radiance", radiance, (N, 3, H, W)),
+                           ("importance", importance, (N, M, H, W)),
+                           ("out", out, (N, 3, H, W))):
+        if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() \
+                or tuple(t.shape) != shape:
+            raise ValueError(f"{name} must be a contiguous float32 CPU tensor of shape {shape}")
+    if blend is not None and (blend.device.type != "cpu" or tuple(blend.shape) != (N, M, H, W)):
+        raise ValueError("blend must be a contiguous float32 CPU tensor [N,M,H,W]")
+    if workspace.device.type != "cuda":
+        raise ValueError("workspace must be a CUDA tensor")
+    cfg = make_config(sizes, blend_is_logits)
+    if stream is None:
+        stream = torch.cuda.current_stream(workspace.device)
+    _check(lib().kmd_decode_filter_fuse_host(
+        radiance.data_ptr(), importance.data_ptr(),
+        None if blend is None else blend.data_ptr(), out.data_ptr(), N, H, W,
+        ctypes.byref(cfg), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        stream.cuda_stream))
+    return out
+
+
+def algorithmic_bytes(N: int, H: int, W: int, sizes: Sequence[int], has_blend: bool) -> int:
+    cfg = make_config(sizes)
+    return int(lib().kmd_algorithmic_bytes(N, H, W, ctypes.byref(cfg), int(bool(has_blend))))
+
+
+def launches_per_call() -> int:
+    return int(lib().kmd_launches_per_call())
+
+
+def version() -> int:
+    return int(lib().kmd_version())
