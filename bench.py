@@ -323,7 +323,8 @@ def run_kmd(args, rank, world, local):
                "kind": "oracle",
                "sample": f"rows {y0}..{y0 + rows} ({rows * W} px) of frame 0 of the {W}x{H} "
                          f"M={M} workload, fp64 oracle, {dt:.1f} s"}
-        kmd.decode_filter_fuse(*views[0], sizes, stream=stream)
+        r0, i0, b0, o0 = views[0]
+        kmd.decode_filter_fuse(r0, i0, b0, sizes, out=o0, stream=stream)
         torch.cuda.synchronize(dev)
         got = outs[0:1, :, y0:y0 + rows].cpu().numpy().astype(np.float64)
         rel = np.abs(got - ref) / np.where(ref == 0, 1.0, np.abs(ref))

@@ -3,6 +3,7 @@
 // enqueued on the caller's stream.  No per-call allocation.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kmd_kernels.h"
@@ -61,6 +62,8 @@ kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t str
     p.blend_is_logits = cfg->blend_is_logits;
     for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < cfg->num_sizes ? cfg->sizes[i] : 1;
     if (p.M == 1) p.blend = nullptr;  // softmax of one logit is 1 (reading R11)
+    static const int dbg = [] { const char* e = getenv("KMD_DEBUG"); return e ? atoi(e) : 0; }();
+    p.debug = dbg;
     const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
     const int total = p.N;
     for (int n0 = 0; n0 < total; n0 += 65535) {
@@ -70,7 +73,9 @@ kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t str
         q.imp = p.imp + (size_t)n0 * p.M * bplane;
         q.blend = p.blend ? p.blend + (size_t)n0 * p.M * oplane : nullptr;
         q.out = p.out + (size_t)n0 * 3 * oplane;
-        cudaError_t e = kmd::launch_fused_direct(q, stream);
+        cudaError_t e = kmd::tma_supported(q)  ? kmd::launch_fused_tma(q, stream)
+                        : kmd::ws_supported(q) ? kmd::launch_fused_ws(q, stream)
+                                               : kmd::launch_fused_direct(q, stream);
         if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
     }
     return KMD_OK;
@@ -91,9 +96,9 @@ kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance
         kmd_status s = check_cfg(cfg, H, W);
         if (s) return s;
     }
+    if (N == 0) return KMD_OK;  // no-op; pointers of empty tensors may be NULL
     if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
-    if (N == 0) return KMD_OK;
     const size_t plane = (size_t)H * W * sizeof(float);
     const size_t M = (size_t)cfg->num_sizes;
     if (overlaps(out, 3 * N * plane, radiance, 3 * N * plane) ||
@@ -125,9 +130,9 @@ kmd_status kmd_fuse(const float* filtered, const float* blend, float* out, int32
     if (M < 1 || M > KMD_MAX_SIZES) return fail(KMD_ERR_CONFIG, "M=%d not in [1,%d]", M, KMD_MAX_SIZES);
     if (blend_is_logits != 0 && blend_is_logits != 1)
         return fail(KMD_ERR_CONFIG, "blend_is_logits=%d must be 0 or 1", blend_is_logits);
+    if (N == 0) return KMD_OK;
     if (!filtered || !out) return fail(KMD_ERR_NULL, "filtered/out is NULL");
     if (M > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", M);
-    if (N == 0) return KMD_OK;
     const size_t plane = (size_t)H * W * sizeof(float);
     if (overlaps(out, 3 * N * plane, filtered, 3 * (size_t)M * N * plane) ||
         (M > 1 && overlaps(out, 3 * N * plane, blend, (size_t)M * N * plane)))
@@ -163,9 +168,9 @@ kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* impor
             return fail(KMD_ERR_DIM, "halo (%d,%d) smaller than required (%d,%d) for r_max=%d", halo_top,
                         halo_bot, need_top, need_bot, r);
     }
+    if (N == 0) return KMD_OK;
     if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
-    if (N == 0) return KMD_OK;
     const int buf_rows = halo_top + band_rows + halo_bot;
     const size_t bplane = (size_t)buf_rows * W * sizeof(float), oplane = (size_t)band_rows * W * sizeof(float);
     const size_t M = (size_t)cfg->num_sizes;
@@ -200,10 +205,10 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
         kmd_status s = check_cfg(cfg, H, W);
         if (s) return s;
     }
+    if (N == 0) return KMD_OK;
     if (!radiance_host || !importance_host || !out_host || !device_workspace)
         return fail(KMD_ERR_NULL, "a host buffer or the workspace is NULL");
     if (cfg->num_sizes > 1 && !blend_host) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
-    if (N == 0) return KMD_OK;
     const size_t need = kmd_host_workspace_bytes(N, H, W, cfg);
     if (workspace_bytes < need)
         return fail(KMD_ERR_DIM, "workspace %zu bytes < required %zu", workspace_bytes, need);

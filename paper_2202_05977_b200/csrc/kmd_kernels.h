@@ -7,6 +7,14 @@ namespace kmd {
 // v1: direct separable sums, one CTA per 32x32 tile (kmd_direct.cu)
 cudaError_t launch_fused_direct(FusedParams p, cudaStream_t stream);
 
+// v2: persistent warp-specialised producer/consumer kernel, k <= 13 (kmd_ws.cu)
+bool ws_supported(const FusedParams& p);
+cudaError_t launch_fused_ws(FusedParams p, cudaStream_t stream);
+
+// v3: persistent warp-specialised kernel fed by TMA, k <= 13, W % 4 == 0 (kmd_tma.cu)
+bool tma_supported(const FusedParams& p);
+cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream);
+
 // fusion only, Eq. 5 (kmd_fuse.cu)
 cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
                              int H, int W, int M, int blend_is_logits, cudaStream_t stream);

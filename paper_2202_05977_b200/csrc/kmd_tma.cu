@@ -1,0 +1,530 @@
+// kmd_tma.cu -- v3 fused decode + filter + fuse for sm_100a: persistent,
+// warp-specialised, TMA-fed (kernel sizes k <= 13, M <= 8, W % 4 == 0).
+//
+// Arithmetic.  The weight of neighbour q in Eq. 3 is exp(I(q))
+// for every window containing q ("weight sharing"), so
+// Eq. 3 + Eq. 4 are exactly a ratio of two k x k box sums of the premultiplied
+// field P = (e, e r, e g, e b), e = exp(I):   R^k(p) = box_k(e r)(p) / box_k(e)(p).
+// Box sums are separable and evaluated with the van Herk / Gil-Werman block
+// decomposition for "+": blocks of k field rows, window = suffix(block b) +
+// prefix(block b+1), about 3 adds per output per component, all of
+// non-negative terms (no subtraction, no cancellation), in an order fixed by
+// the window's position in the global tile grid.
+//
+// Per CTA (one per SM), per 52 x 24 output tile, per kernel size i:
+//   warp 0  (TMA)      cp.async.bulk.tensor loads: radiance box [3][36][68]
+//                      (double-buffered per tile), I_i box [36][68] and blend
+//                      box [24][68] into a ring of 3 slots; mbarrier expect_tx.
+//   warps 1-4 (field)  job = (size i, 32-column half): lane = field column;
+//                      e = exp(I) once per field pixel, vertical box sums in
+//                      registers, V[24][64] float4 into the slot.
+//   warps 5-7 (fusion) thread = (row, 13-pixel segment): horizontal box sums of
+//                      V, R = num * rcp(den), online softmax over the blend
+//                      logits (Eq. 5); after the last
+//                      size the tile is staged and written by one TMA store.
+// Clamp-to-edge (reading R1): columns via a per-lane clamped smem column;
+// rows outside the frame are replicated into the TMA zero-filled box rows by
+// the field warps of border tiles.  Pixels whose box denominators leave
+// [1e-30, 1e36] (or whose result is not finite) are recomputed exactly with a
+// per-window max shift (reading R2/R13).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "kmd_common.cuh"
+#include "kmd_kernels.h"
+
+namespace kmd {
+namespace tma {
+
+constexpr int RMAX = 6;
+constexpr int TW = 52;              // output columns per tile
+constexpr int FW = TW + 2 * RMAX;   // 64 field columns (2 warps), global x0-6 .. x0+57
+constexpr int TH = 24;              // output rows per tile
+constexpr int FH = TH + 2 * RMAX;   // 36 field rows in every box
+// Every TMA box starts at column x0-8: the innermost box coordinate must be a
+// multiple of 16 bytes when it is negative (measured on this B200: -6 faults,
+// -8 works), and 68 columns cover x0-6 .. x0+57 (and the 52 output columns).
+constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
+constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
+constexpr int VS = 68;
+constexpr int SEG = 13;             // pixels per fusion thread
+constexpr int NS = 3;               // slots
+constexpr int NFIELD = 4;           // field warps
+constexpr int NFUSE = 3;            // fusion warps (TH * 4 segments = 96 threads)
+constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
+constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
+constexpr float L2E_LO = 1.925963033500011079e-08f;       // log2(e) - L2E
+constexpr float LN2 = 0.693147180559945309f;
+
+struct Slot {
+    float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
+    alignas(128) float B[TH][BW];      // blend logits of map i, rows y0 .. y0+23, cols x0-8 .. x0+59
+    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
+};
+struct RadBuf {
+    alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
+};
+struct Smem {
+    RadBuf rad[2];
+    Slot slot[NS];
+    float stage[3][TH][TW];
+    unsigned long long rad_full[2], rad_empty[2], in_full[NS], v_full[NS], slot_empty[NS];
+};
+static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0, "TMA destinations 128-B aligned");
+
+// ------------------------------------------------------------------ TMA PTX
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
+
+// exp(x) = 2^(x log2 e) with the product's rounding error carried to first
+// order: t = fl(x L2E), c = (x L2E - t) + x L2E_LO, e = 2^t (1 + c ln 2).
+// ~2-3 ulp for |x| <= 88 (MUFU.EX2 + 5 FP32 ops).
+__device__ __forceinline__ float exp_acc(float x) {
+    const float t = x * L2E;
+    const float c = fmaf(x, L2E_LO, fmaf(x, L2E, -t));
+    const float e = ex2_approx(t);
+    return fmaf(e * c, LN2, e);
+}
+
+// ---- Gil-Werman box sums along one line ----------------------------------
+// out[x] = sum_{j=x}^{x+2R} P[j] for x in [0, N); P produced by field(j) for
+// j in [0, N + 2R), each exactly once.  Blocks of k = 2R+1 field values:
+// suf = suffix sums of block b; window x = bk + t is suf[t] + prefix_{b+1}[t-1].
+template <int R, int N, int B, class F, class E>
+__device__ __forceinline__ void gw_block(float4 (&suf)[2 * R + 1], F& field, E& emit) {
+    constexpr int K = 2 * R + 1;
+    constexpr int X0 = B * K;
+    if constexpr (X0 < N) {
+        emit(X0, suf[0]);
+        constexpr int TMAX = (K - 1 < N - 1 - X0) ? K - 1 : N - 1 - X0;  // outputs X0+1 .. X0+TMAX
+        constexpr bool NEXT = X0 + K < N;
+        constexpr int NROWS = NEXT ? K : TMAX;
+        float4 raw[K];
+#pragma unroll
+        for (int t = 0; t < NROWS; ++t) raw[t] = field((B + 1) * K + t);
+        float4 pre = raw[0];
+#pragma unroll
+        for (int t = 1; t <= TMAX; ++t) {
+            if (t > 1) pre = add4(pre, raw[t - 1]);
+            emit(X0 + t, add4(suf[t], pre));
+        }
+        if constexpr (NEXT) {
+#pragma unroll
+            for (int t = K - 2; t >= 0; --t) raw[t] = add4(raw[t], raw[t + 1]);
+            gw_block<R, N, B + 1>(raw, field, emit);
+        }
+    }
+}
+
+template <int R, int N, class F, class E>
+__device__ __forceinline__ void gw_line(F&& field, E&& emit) {
+    constexpr int K = 2 * R + 1;
+    float4 suf[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) suf[t] = field(t);
+#pragma unroll
+    for (int t = K - 2; t >= 0; --t) suf[t] = add4(suf[t], suf[t + 1]);
+    gw_block<R, N, 0>(suf, field, emit);
+}
+
+struct Tile {
+    int n, x0, y0;
+};
+
+__device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x, int tiles_y) {
+    Tile c;
+    const int per_frame = tiles_x * tiles_y;
+    c.n = t / per_frame;
+    const int r = t - c.n * per_frame;
+    const int ty = r / tiles_x;
+    c.x0 = (r - ty * tiles_x) * TW;
+    c.y0 = p.tile_y_begin + ty * TH;
+    return c;
+}
+
+// rows of the box (global y0-6 .. y0+29) outside the frame/buffer take the
+// value of the nearest valid row (clamp-to-edge, reading R1)
+__device__ __forceinline__ void fix_rows(float* col, int plane_stride, int nplanes, int top, int bot) {
+    for (int pl = 0; pl < nplanes; ++pl) {
+        float* c = col + pl * plane_stride;
+        if (top > 0) {
+            const float v = c[top * BW];
+            for (int r = 0; r < top; ++r) c[r * BW] = v;
+        }
+        if (bot < FH) {
+            const float v = c[(bot - 1) * BW];
+            for (int r = bot; r < FH; ++r) c[r * BW] = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------ field warps
+template <int R>
+__device__ __forceinline__ void field_job(Smem& sm, Slot& sl, int rb, int h, int cc) {
+    const int c = h * 32 + (threadIdx.x & 31);
+    const float* Ib = &sl.I[RMAX - R][cc];
+    const float* Rb = &sm.rad[rb].v[0][RMAX - R][cc];
+    float4* Vc = &sl.V[0][c];
+    gw_line<R, TH>(
+        [&](int f) {
+            const float v = Ib[f * BW];
+            const float r = Rb[f * BW], g = Rb[FH * BW + f * BW], b = Rb[2 * FH * BW + f * BW];
+            const float e = exp_acc(v);  // once per field pixel (Eq. 3's shared weight)
+            const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(g, b));  // pairs (e, er), (eg, eb)
+            return make_float4(e, e * r, gb.x, gb.y);
+        },
+        [&](int oy, float4 v) {
+            // two 8-byte stores keep the FADD2 register pairs in place (no MOVs
+            // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
+            const unsigned a = smem_u32(&Vc[oy * VS]);
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+            asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
+        });
+}
+
+// --------------------------------------------------------------- fusion warps
+struct Acc {
+    float m[SEG], S[SEG], a[SEG][3];
+    unsigned bad;
+};
+
+__device__ __forceinline__ void fuse_px(const FusedParams& p, Acc& st, int j, float b, float4 v) {
+    const float den = v.x;
+    st.bad |= (den >= 1e-30f && den <= 1e36f) ? 0u : (1u << j);
+    const float rden = rcp_approx(den);
+    if (p.M == 1) {
+        st.a[j][0] = v.y * rden;
+        st.a[j][1] = v.z * rden;
+        st.a[j][2] = v.w * rden;
+    } else if (p.blend_is_logits) {
+        const float mn = fmaxf(st.m[j], b);
+        const float cold = ex2_approx((st.m[j] - mn) * L2E);
+        const float a = ex2_approx((b - mn) * L2E);
+        st.m[j] = mn;
+        st.S[j] = fmaf(st.S[j], cold, a);
+        const float w = a * rden;
+        st.a[j][0] = fmaf(st.a[j][0], cold, w * v.y);
+        st.a[j][1] = fmaf(st.a[j][1], cold, w * v.z);
+        st.a[j][2] = fmaf(st.a[j][2], cold, w * v.w);
+    } else {
+        const float w = b * rden;
+        st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
+        st.a[j][1] = fmaf(w, v.z, st.a[j][1]);
+        st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, Acc& st, int ty, int seg) {
+    const float4* Vr = &sl.V[ty][SEG * seg + RMAX - R];
+    const float* Br = &sl.B[ty][SEG * seg + XOFF];
+    gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { fuse_px(p, st, x, Br[x], v); });
+}
+
+// Exact per-pixel evaluation of Eq. 3-5 with per-window max shifts (R2), for
+// the rare pixels whose unshifted box sums left the safe range.
+__device__ __noinline__ float3 exact_pixel(const FusedParams& p, int n, int x, int y) {
+    const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
+    const float* rp = p.rad + (size_t)n * 3 * bplane;
+    float mb = -INFINITY;
+    if (p.M > 1 && p.blend_is_logits)
+        for (int i = 0; i < p.M; ++i)
+            mb = fmaxf(mb, p.blend[((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x]);
+    float S = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f;
+    for (int i = 0; i < p.M; ++i) {
+        const int R = (p.sizes[i] - 1) / 2;
+        const float* Ii = p.imp + ((size_t)n * p.M + i) * bplane;
+        auto off = [&](int dy, int dx) {
+            const int gy = clampi(clampi(y + dy, 0, p.H - 1) - p.row_base, 0, p.buf_rows - 1);
+            return (size_t)gy * p.W + clampi(x + dx, 0, p.W - 1);
+        };
+        float m = -INFINITY;
+        for (int dy = -R; dy <= R; ++dy)
+            for (int dx = -R; dx <= R; ++dx) m = fmaxf(m, Ii[off(dy, dx)]);
+        float den = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
+        for (int dy = -R; dy <= R; ++dy)
+            for (int dx = -R; dx <= R; ++dx) {
+                const size_t q = off(dy, dx);
+                const float e = expf(Ii[q] - m);
+                den += e;
+                n0 = fmaf(e, rp[q], n0);
+                n1 = fmaf(e, rp[bplane + q], n1);
+                n2 = fmaf(e, rp[2 * bplane + q], n2);
+            }
+        float a = 1.f;
+        if (p.M > 1) {
+            const float b = p.blend[((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x];
+            a = p.blend_is_logits ? expf(b - mb) : b;
+        }
+        S += a;
+        o0 = fmaf(a, n0 / den, o0);
+        o1 = fmaf(a, n1 / den, o1);
+        o2 = fmaf(a, n2 / den, o2);
+    }
+    if (p.M > 1 && p.blend_is_logits) {
+        o0 /= S;
+        o1 /= S;
+        o2 /= S;
+    }
+    return make_float3(o0, o1, o2);
+}
+
+// --------------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(NTHREADS, 1)
+    fused_tma_kernel(const __grid_constant__ FusedParams p, const __grid_constant__ CUtensorMap tm_rad,
+                     const __grid_constant__ CUtensorMap tm_imp, const __grid_constant__ CUtensorMap tm_blend,
+                     const __grid_constant__ CUtensorMap tm_out, int tiles_x, int tiles_y, int n_tiles) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int M = p.M;
+    const bool has_blend = p.blend != nullptr && !(p.debug & 16);
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sm.rad_full[b], 1);
+            mbar_init(&sm.rad_empty[b], NFIELD);
+        }
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&sm.in_full[s], 1);
+            mbar_init(&sm.v_full[s], 2 * 32);
+            mbar_init(&sm.slot_empty[s], NFUSE * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------- TMA
+        if (lane == 0) {
+            if (!(p.debug & 8)) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
+            }
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BW * 4;
+            auto load_rad = [&](int tl) {
+                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                const int rb = tl & 1;
+                mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.rad_full[rb], RAD_BYTES);
+                tma_load_3d(&sm.rad[rb].v[0][0][0], &tm_rad, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base, tc.n * 3,
+                            &sm.rad_full[rb]);
+            };
+            if (my_tiles > 0) load_rad(0);
+            for (int tl = 0; tl < my_tiles; ++tl) {
+                if (tl + 1 < my_tiles) load_rad(tl + 1);
+                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                for (int i = 0; i < M; ++i) {
+                    const int seq = tl * M + i, s = seq % NS;
+                    mbar_wait(&sm.slot_empty[s], ((seq / NS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES + (has_blend ? B_BYTES : 0u));
+                    tma_load_3d(&sm.slot[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
+                                tc.n * M + i, &sm.in_full[s]);
+                    if (has_blend)
+                        tma_load_3d(&sm.slot[s].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
+                                    &sm.in_full[s]);
+                }
+            }
+        }
+    } else if (warp <= NFIELD) {
+        // ----------------------------------------------------------- field
+        const int fw = warp - 1;
+        const int ylo = max(0, p.row_base), yhi = min(p.H, p.row_base + p.buf_rows) - 1;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+            const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            const int rb = tl & 1;
+            const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
+            const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
+            const bool border_rows = top > 0 || bot < FH;
+            mbar_wait(&sm.rad_full[rb], (tl >> 1) & 1);
+            for (int jl = fw; jl < 2 * M; jl += NFIELD) {
+                const int i = jl >> 1, h = jl & 1;
+                const int seq = tl * M + i, s = seq % NS;
+                const int c = h * 32 + lane;
+                const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
+                mbar_wait(&sm.in_full[s], (seq / NS) & 1);
+                Slot& sl = sm.slot[s];
+                if (border_rows && !(p.debug & 4)) {
+                    fix_rows(&sl.I[0][cc], FH * BW, 1, top, bot);
+                    fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
+                    fence_proxy_async();  // generic writes before the next TMA overwrite
+                }
+                if (!(p.debug & 32)) switch ((p.sizes[i] - 1) / 2) {
+                    case 0: field_job<0>(sm, sl, rb, h, cc); break;
+                    case 1: field_job<1>(sm, sl, rb, h, cc); break;
+                    case 2: field_job<2>(sm, sl, rb, h, cc); break;
+                    case 3: field_job<3>(sm, sl, rb, h, cc); break;
+                    case 4: field_job<4>(sm, sl, rb, h, cc); break;
+                    case 5: field_job<5>(sm, sl, rb, h, cc); break;
+                    default: field_job<6>(sm, sl, rb, h, cc); break;
+                }
+                mbar_arrive(&sm.v_full[s]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.rad_empty[rb]);
+        }
+    } else {
+        // ----------------------------------------------------------- fusion
+        const int c = threadIdx.x - (1 + NFIELD) * 32;
+        const int ty = c >> 2, seg = c & 3;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+            const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            Acc st;
+            st.bad = 0;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                st.m[j] = -INFINITY;
+                st.S[j] = 0.f;
+                st.a[j][0] = st.a[j][1] = st.a[j][2] = 0.f;
+            }
+            for (int i = 0; i < M; ++i) {
+                const int seq = tl * M + i, s = seq % NS;
+                mbar_wait(&sm.v_full[s], (seq / NS) & 1);
+                const Slot& sl = sm.slot[s];
+                if (!(p.debug & 64)) switch ((p.sizes[i] - 1) / 2) {
+                    case 0: fuse_job<0>(p, sl, st, ty, seg); break;
+                    case 1: fuse_job<1>(p, sl, st, ty, seg); break;
+                    case 2: fuse_job<2>(p, sl, st, ty, seg); break;
+                    case 3: fuse_job<3>(p, sl, st, ty, seg); break;
+                    case 4: fuse_job<4>(p, sl, st, ty, seg); break;
+                    case 5: fuse_job<5>(p, sl, st, ty, seg); break;
+                    default: fuse_job<6>(p, sl, st, ty, seg); break;
+                }
+                mbar_arrive(&sm.slot_empty[s]);
+            }
+            // ---- normalise, exact fallback for flagged pixels, stage, TMA store
+            if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
+            fuse_bar();
+            const int gy = tc.y0 + ty;
+            const bool row_ok = gy >= p.out_y0 && gy < p.out_y0 + p.out_rows;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const float sc = (M > 1 && p.blend_is_logits) ? rcp_approx(st.S[j]) : 1.0f;
+                float o0 = st.a[j][0] * sc, o1 = st.a[j][1] * sc, o2 = st.a[j][2] * sc;
+                const int gx = tc.x0 + SEG * seg + j;
+                const bool bad = ((st.bad >> j) & 1u) || !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
+                if (bad && row_ok && gx < p.W && !(p.debug & 2)) {
+                    const float3 e = exact_pixel(p, tc.n, gx, gy);
+                    o0 = e.x;
+                    o1 = e.y;
+                    o2 = e.z;
+                }
+                sm.stage[0][ty][SEG * seg + j] = o0;
+                sm.stage[1][ty][SEG * seg + j] = o1;
+                sm.stage[2][ty][SEG * seg + j] = o2;
+            }
+            fence_proxy_async();
+            fuse_bar();
+            if (tc.y0 >= p.out_y0) {
+                // TMA store; it clips the parts beyond W / out_rows.  (A TMA store
+                // with a negative coordinate faults on this B200, so the first tile
+                // of a row band that starts inside a tile is stored by hand below.)
+                if (c == 0 && !(p.debug & 1)) tma_store_3d(&tm_out, tc.x0, tc.y0 - p.out_y0, tc.n * 3, &sm.stage[0][0][0]);
+            } else {
+                float* out = p.out + (size_t)tc.n * 3 * ((size_t)p.out_rows * p.W);
+                for (int idx = c; idx < 3 * TH * TW; idx += NFUSE * 32) {
+                    const int ch = idx / (TH * TW), rr = idx - ch * TH * TW;
+                    const int oy = rr / TW, ox = rr - oy * TW;
+                    const int yy = tc.y0 + oy, xx = tc.x0 + ox;
+                    if (xx < p.W && yy >= p.out_y0 && yy < p.out_y0 + p.out_rows)
+                        out[((size_t)ch * p.out_rows + (yy - p.out_y0)) * p.W + xx] = sm.stage[ch][oy][ox];
+                }
+            }
+        }
+        if (c == 0) bulk_wait0();
+    }
+}
+
+// ------------------------------------------------------------------- host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long planes, int bw, int bh, int bp) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * 4 * rows};
+    const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bp};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace tma
+
+bool tma_supported(const FusedParams& p) {
+    if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % 4 != 0) return false;
+    for (int i = 0; i < p.M; ++i)
+        if ((p.sizes[i] - 1) / 2 > tma::RMAX) return false;
+    const uintptr_t a = (uintptr_t)p.rad | (uintptr_t)p.imp | (uintptr_t)p.out | (uintptr_t)p.blend;
+    if (a & 15) return false;
+    return tma::get_encode() != nullptr;
+}
+
+cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
+    using namespace tma;
+    p.tile_y_begin = (p.out_y0 / TH) * TH;
+    const int tiles_y = (p.out_y0 + p.out_rows - p.tile_y_begin + TH - 1) / TH;
+    const int tiles_x = (p.W + TW - 1) / TW;
+    const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
+    if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
+    CUtensorMap m_rad, m_imp, m_blend, m_out;
+    if (!make_map(&m_rad, p.rad, p.W, p.buf_rows, 3LL * p.N, BW, FH, 3) ||
+        !make_map(&m_imp, p.imp, p.W, p.buf_rows, (long long)p.M * p.N, BW, FH, 1) ||
+        !make_map(&m_out, p.out, p.W, p.out_rows, 3LL * p.N, TW, TH, 3))
+        return cudaErrorInvalidValue;
+    if (p.blend) {
+        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BW, TH, 1))
+            return cudaErrorInvalidValue;
+    } else {
+        m_blend = m_imp;  // never used
+    }
+    int dev = 0, sms = 148;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err != cudaSuccess) return err;
+    const size_t smem = sizeof(Smem);
+    err = cudaFuncSetAttribute(fused_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    const int grid = (int)(n_tiles < sms ? n_tiles : sms);
+    fused_tma_kernel<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y,
+                                                       (int)n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace kmd

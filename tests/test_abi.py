@@ -75,8 +75,9 @@ def test_null_dim_alias_errors(L, kmdmod):
     assert _call(L, kmdmod, [3], out=0x1000 + 64) == 5   # out overlaps radiance
     assert _call(L, kmdmod, [3, 5], out=0x200000 + 4) == 5  # out overlaps blend
     cfg = kmdmod.make_config([3])
-    assert L.kmd_decode_filter_fuse(None, None, None, None, 0, 0, 0, ctypes.byref(cfg), None) == 1
-    assert L.kmd_decode_filter_fuse(0x10, 0x20, None, 0x30, 0, 0, 0, ctypes.byref(cfg), None) == 0
+    # N == 0 is a no-op (empty tensors have NULL data pointers)
+    assert L.kmd_decode_filter_fuse(None, None, None, None, 0, 0, 0, ctypes.byref(cfg), None) == 0
+    assert L.kmd_decode_filter_fuse(None, 0x20, None, 0x30, 1, 8, 8, ctypes.byref(cfg), None) == 1
 
 
 def test_band_geometry_errors(L, kmdmod):
@@ -87,8 +88,7 @@ def test_band_geometry_errors(L, kmdmod):
     assert f(*args, 1, 100, 64, 5, 6, 100, 400, ctypes.byref(cfg), None) == 3
     # band beyond the frame
     assert f(*args, 1, 100, 64, 6, 6, 300, 400, ctypes.byref(cfg), None) == 3
-    # top band needs no top halo; bottom halo of 6 OK (checks pass, so only the
-    # CUDA launch would remain -- not exercised here)
+    # bottom halo 5 < r_max = 6 for a band that does not reach the frame bottom
     assert f(*args, 1, 100, 64, 0, 5, 0, 400, ctypes.byref(cfg), None) == 3
 
 
