@@ -59,6 +59,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         : "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
     const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));

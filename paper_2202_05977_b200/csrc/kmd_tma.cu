@@ -13,11 +13,14 @@
 //
 // Per CTA (one per SM), per 52 x 24 output tile, per kernel size i:
 //   warp 0  (TMA)      cp.async.bulk.tensor loads: radiance box [3][36][68]
-//                      (double-buffered per tile), I_i box [36][68] and blend
-//                      box [24][68] into a ring of 3 slots; mbarrier expect_tx.
+//                      (double-buffered per tile) and the I_i box [36][68]
+//                      into a 5-deep input ring (mbarrier expect_tx), running
+//                      ahead of the compute by up to 5 (tile, size) steps.
 //   warps 1-4 (field)  job = (size i, 32-column half): lane = field column;
 //                      e = exp(I) once per field pixel, vertical box sums in
-//                      registers, V[24][64] float4 into the slot.
+//                      registers, V[24][64] float4 into a 3-deep V ring; the
+//                      half-0 warp also TMA-loads the blend box [24][68] of
+//                      size i next to its V.
 //   warps 5-7 (fusion) thread = (row, 13-pixel segment): horizontal box sums of
 //                      V, R = num * rcp(den), online softmax over the blend
 //                      logits (Eq. 5); after the last
@@ -49,7 +52,8 @@ constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
 constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
 constexpr int VS = 68;
 constexpr int SEG = 13;             // pixels per fusion thread
-constexpr int NS = 3;               // slots
+constexpr int NI = 5;               // input (importance) ring depth
+constexpr int NV = 3;               // V ring depth (field -> fusion)
 constexpr int NFIELD = 4;           // field warps
 constexpr int NFUSE = 3;            // fusion warps (TH * 4 segments = 96 threads)
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
@@ -57,21 +61,25 @@ constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to f
 constexpr float L2E_LO = 1.925963033500011079e-08f;       // log2(e) - L2E
 constexpr float LN2 = 0.693147180559945309f;
 
+struct InSlot {
+    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
+};
 struct Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
     alignas(128) float B[TH][BW];      // blend logits of map i, rows y0 .. y0+23, cols x0-8 .. x0+59
-    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
 };
 struct RadBuf {
     alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
 };
 struct Smem {
     RadBuf rad[2];
-    Slot slot[NS];
+    InSlot in[NI];
+    Slot slot[NV];
     float stage[3][TH][TW];
-    unsigned long long rad_full[2], rad_empty[2], in_full[NS], v_full[NS], slot_empty[NS];
+    unsigned long long rad_full[2], rad_empty[2], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV];
 };
-static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0, "TMA destinations 128-B aligned");
+static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlot) % 128 == 0,
+              "TMA destinations 128-B aligned");
 
 // ------------------------------------------------------------------ TMA PTX
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
@@ -178,9 +186,9 @@ __device__ __forceinline__ void fix_rows(float* col, int plane_stride, int nplan
 
 // ------------------------------------------------------------ field warps
 template <int R>
-__device__ __forceinline__ void field_job(Smem& sm, Slot& sl, int rb, int h, int cc) {
+__device__ __forceinline__ void field_job(Smem& sm, const InSlot& in, Slot& sl, int rb, int h, int cc) {
     const int c = h * 32 + (threadIdx.x & 31);
-    const float* Ib = &sl.I[RMAX - R][cc];
+    const float* Ib = &in.I[RMAX - R][cc];
     const float* Rb = &sm.rad[rb].v[0][RMAX - R][cc];
     float4* Vc = &sl.V[0][c];
     gw_line<R, TH>(
@@ -202,41 +210,73 @@ __device__ __forceinline__ void field_job(Smem& sm, Slot& sl, int rb, int h, int
 
 // --------------------------------------------------------------- fusion warps
 struct Acc {
-    float m[SEG], S[SEG], a[SEG][3];
-    unsigned bad;
+    float b0[SEG], S[SEG], a[SEG][3], dmin[SEG], dmax[SEG];
 };
 
-__device__ __forceinline__ void fuse_px(const FusedParams& p, Acc& st, int j, float b, float4 v) {
+// Eq. 5 with alpha = softmax(B), accumulated one size
+// at a time.  The softmax is shifted by the first size's logit b0 (any shift
+// is exact, reading R2): a_i = exp(B_i - b0) with a_0 = 1, so S >= 1; an
+// overflow (B_i - b0 > 88) makes the pixel non-finite and sends it to the
+// exact path.  den range is tracked for the same check (reading R13).
+enum { FUSE_ONE = 0, FUSE_FIRST = 1, FUSE_LOGIT = 2, FUSE_ALPHA = 3 };
+
+template <int MODE>
+__device__ __forceinline__ void fuse_px(Acc& st, int j, float b, float4 v) {
     const float den = v.x;
-    st.bad |= (den >= 1e-30f && den <= 1e36f) ? 0u : (1u << j);
+    st.dmin[j] = fminf(st.dmin[j], den);
+    st.dmax[j] = fmaxf(st.dmax[j], den);
     const float rden = rcp_approx(den);
-    if (p.M == 1) {
-        st.a[j][0] = v.y * rden;
-        st.a[j][1] = v.z * rden;
-        st.a[j][2] = v.w * rden;
-    } else if (p.blend_is_logits) {
-        const float mn = fmaxf(st.m[j], b);
-        const float cold = ex2_approx((st.m[j] - mn) * L2E);
-        const float a = ex2_approx((b - mn) * L2E);
-        st.m[j] = mn;
-        st.S[j] = fmaf(st.S[j], cold, a);
-        const float w = a * rden;
-        st.a[j][0] = fmaf(st.a[j][0], cold, w * v.y);
-        st.a[j][1] = fmaf(st.a[j][1], cold, w * v.z);
-        st.a[j][2] = fmaf(st.a[j][2], cold, w * v.w);
-    } else {
-        const float w = b * rden;
-        st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
-        st.a[j][1] = fmaf(w, v.z, st.a[j][1]);
-        st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
+    float w;
+    if constexpr (MODE == FUSE_ONE) {
+        w = rden;
+    } else if constexpr (MODE == FUSE_FIRST) {  // a_0 = exp(B_0 - b0) = 1
+        st.b0[j] = b;
+        st.S[j] += 1.0f;
+        w = rden;
+    } else if constexpr (MODE == FUSE_LOGIT) {
+        const float a = exp_acc(b - st.b0[j]);
+        st.S[j] += a;
+        w = a * rden;
+    } else {  // alpha given (blend_is_logits == 0)
+        w = b * rden;
     }
+    st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
+    st.a[j][1] = fmaf(w, v.z, st.a[j][1]);
+    st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
 }
 
+template <int MODE>
+__device__ __forceinline__ void fuse_seg(Acc& st, const float* Br, const float4 (&o)[SEG]) {
+#pragma unroll
+    for (int j = 0; j < SEG; ++j) fuse_px<MODE>(st, j, Br[j], o[j]);
+}
+
+// Horizontal box sums of one size for the thread's 13 pixels (templated on
+// the radius: only this part differs between sizes, so the fusion code that
+// follows exists once -- keeps the fusion warps' hot code small).
 template <int R>
-__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, Acc& st, int ty, int seg) {
+__device__ __forceinline__ void hbox(const Slot& sl, int ty, int seg, float4 (&o)[SEG]) {
     const float4* Vr = &sl.V[ty][SEG * seg + RMAX - R];
+    gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
+}
+
+__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, Acc& st, int ty, int seg, int R,
+                                         int i) {
+    float4 o[SEG];
+    switch (R) {
+        case 0: hbox<0>(sl, ty, seg, o); break;
+        case 1: hbox<1>(sl, ty, seg, o); break;
+        case 2: hbox<2>(sl, ty, seg, o); break;
+        case 3: hbox<3>(sl, ty, seg, o); break;
+        case 4: hbox<4>(sl, ty, seg, o); break;
+        case 5: hbox<5>(sl, ty, seg, o); break;
+        default: hbox<6>(sl, ty, seg, o); break;
+    }
     const float* Br = &sl.B[ty][SEG * seg + XOFF];
-    gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { fuse_px(p, st, x, Br[x], v); });
+    if (p.M == 1) fuse_seg<FUSE_ONE>(st, Br, o);
+    else if (!p.blend_is_logits) fuse_seg<FUSE_ALPHA>(st, Br, o);
+    else if (i == 0) fuse_seg<FUSE_FIRST>(st, Br, o);
+    else fuse_seg<FUSE_LOGIT>(st, Br, o);
 }
 
 // Exact per-pixel evaluation of Eq. 3-5 with per-window max shifts (R2), for
@@ -303,10 +343,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&sm.rad_full[b], 1);
             mbar_init(&sm.rad_empty[b], NFIELD);
         }
-        for (int s = 0; s < NS; ++s) {
+        for (int s = 0; s < NI; ++s) {
             mbar_init(&sm.in_full[s], 1);
-            mbar_init(&sm.v_full[s], 2 * 32);
-            mbar_init(&sm.slot_empty[s], NFUSE * 32);
+            mbar_init(&sm.in_empty[s], 2 * 32);         // both halves, every lane
+        }
+        for (int s = 0; s < NV; ++s) {
+            mbar_init(&sm.v_full[s], 2 * 32 + 1);       // both halves + the blend expect_tx
+            mbar_init(&sm.v_empty[s], NFUSE * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -320,29 +363,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
-            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BW * 4;
-            auto load_rad = [&](int tl) {
-                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
-                const int rb = tl & 1;
-                mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sm.rad_full[rb], RAD_BYTES);
-                tma_load_3d(&sm.rad[rb].v[0][0][0], &tm_rad, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base, tc.n * 3,
-                            &sm.rad_full[rb]);
-            };
-            if (my_tiles > 0) load_rad(0);
-            for (int tl = 0; tl < my_tiles; ++tl) {
-                if (tl + 1 < my_tiles) load_rad(tl + 1);
-                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
-                for (int i = 0; i < M; ++i) {
-                    const int seq = tl * M + i, s = seq % NS;
-                    mbar_wait(&sm.slot_empty[s], ((seq / NS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES + (has_blend ? B_BYTES : 0u));
-                    tma_load_3d(&sm.slot[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
-                                tc.n * M + i, &sm.in_full[s]);
-                    if (has_blend)
-                        tma_load_3d(&sm.slot[s].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
-                                    &sm.in_full[s]);
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4;
+            // Issue whichever load is ready first: the next tile's radiance
+            // (needs the field warps to be done with tile tl-1) or the next
+            // importance box (needs a free input slot).  Polling with test_wait
+            // keeps the importance ring full across tile boundaries.
+            int next_rad = 0, next_seq = 0;
+            const int total_seq = my_tiles * M;
+            while (next_rad < my_tiles || next_seq < total_seq) {
+                const bool rad_due = next_rad < my_tiles && next_rad <= next_seq / M + 1;
+                if (rad_due && mbar_test(&sm.rad_empty[next_rad & 1], ((next_rad >> 1) & 1) ^ 1)) {
+                    const Tile tc = tile_of(p, blockIdx.x + next_rad * gridDim.x, tiles_x, tiles_y);
+                    const int rb = next_rad & 1;
+                    mbar_arrive_expect_tx(&sm.rad_full[rb], RAD_BYTES);
+                    tma_load_3d(&sm.rad[rb].v[0][0][0], &tm_rad, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base, tc.n * 3,
+                                &sm.rad_full[rb]);
+                    ++next_rad;
+                    continue;
                 }
+                if (next_seq < total_seq) {
+                    const int s = next_seq % NI;
+                    if (mbar_test(&sm.in_empty[s], ((next_seq / NI) & 1) ^ 1)) {
+                        const int tl = next_seq / M, i = next_seq - tl * M;
+                        const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                        mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES);
+                        tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
+                                    tc.n * M + i, &sm.in_full[s]);
+                        ++next_seq;
+                        continue;
+                    }
+                }
+                __nanosleep(64);  // nothing ready: back off instead of stealing issue slots
             }
         }
     } else if (warp <= NFIELD) {
@@ -358,26 +409,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_wait(&sm.rad_full[rb], (tl >> 1) & 1);
             for (int jl = fw; jl < 2 * M; jl += NFIELD) {
                 const int i = jl >> 1, h = jl & 1;
-                const int seq = tl * M + i, s = seq % NS;
+                const int seq = tl * M + i, si = seq % NI, sv = seq % NV;
                 const int c = h * 32 + lane;
                 const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
-                mbar_wait(&sm.in_full[s], (seq / NS) & 1);
-                Slot& sl = sm.slot[s];
+                Slot& sl = sm.slot[sv];
+                InSlot& in = sm.in[si];
+                mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);  // V slot (and its blend box) free
+                if (h == 0 && lane == 0) {
+                    mbar_arrive_expect_tx(&sm.v_full[sv], has_blend ? TH * BW * 4 : 0u);
+                    if (has_blend)
+                        tma_load_3d(&sl.B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
+                                    &sm.v_full[sv]);
+                }
+                mbar_wait(&sm.in_full[si], (seq / NI) & 1);
                 if (border_rows && !(p.debug & 4)) {
-                    fix_rows(&sl.I[0][cc], FH * BW, 1, top, bot);
+                    fix_rows(&in.I[0][cc], FH * BW, 1, top, bot);
                     fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
                     fence_proxy_async();  // generic writes before the next TMA overwrite
                 }
                 if (!(p.debug & 32)) switch ((p.sizes[i] - 1) / 2) {
-                    case 0: field_job<0>(sm, sl, rb, h, cc); break;
-                    case 1: field_job<1>(sm, sl, rb, h, cc); break;
-                    case 2: field_job<2>(sm, sl, rb, h, cc); break;
-                    case 3: field_job<3>(sm, sl, rb, h, cc); break;
-                    case 4: field_job<4>(sm, sl, rb, h, cc); break;
-                    case 5: field_job<5>(sm, sl, rb, h, cc); break;
-                    default: field_job<6>(sm, sl, rb, h, cc); break;
+                    case 0: field_job<0>(sm, in, sl, rb, h, cc); break;
+                    case 1: field_job<1>(sm, in, sl, rb, h, cc); break;
+                    case 2: field_job<2>(sm, in, sl, rb, h, cc); break;
+                    case 3: field_job<3>(sm, in, sl, rb, h, cc); break;
+                    case 4: field_job<4>(sm, in, sl, rb, h, cc); break;
+                    case 5: field_job<5>(sm, in, sl, rb, h, cc); break;
+                    default: field_job<6>(sm, in, sl, rb, h, cc); break;
                 }
-                mbar_arrive(&sm.v_full[s]);
+                mbar_arrive(&sm.in_empty[si]);
+                mbar_arrive(&sm.v_full[sv]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.rad_empty[rb]);
@@ -389,48 +449,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             Acc st;
-            st.bad = 0;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
-                st.m[j] = -INFINITY;
+                st.b0[j] = 0.f;
                 st.S[j] = 0.f;
                 st.a[j][0] = st.a[j][1] = st.a[j][2] = 0.f;
+                st.dmin[j] = INFINITY;
+                st.dmax[j] = 0.f;
             }
             for (int i = 0; i < M; ++i) {
-                const int seq = tl * M + i, s = seq % NS;
-                mbar_wait(&sm.v_full[s], (seq / NS) & 1);
+                const int seq = tl * M + i, s = seq % NV;
+                mbar_wait(&sm.v_full[s], (seq / NV) & 1);
                 const Slot& sl = sm.slot[s];
-                if (!(p.debug & 64)) switch ((p.sizes[i] - 1) / 2) {
-                    case 0: fuse_job<0>(p, sl, st, ty, seg); break;
-                    case 1: fuse_job<1>(p, sl, st, ty, seg); break;
-                    case 2: fuse_job<2>(p, sl, st, ty, seg); break;
-                    case 3: fuse_job<3>(p, sl, st, ty, seg); break;
-                    case 4: fuse_job<4>(p, sl, st, ty, seg); break;
-                    case 5: fuse_job<5>(p, sl, st, ty, seg); break;
-                    default: fuse_job<6>(p, sl, st, ty, seg); break;
-                }
-                mbar_arrive(&sm.slot_empty[s]);
+                if (!(p.debug & 64)) fuse_job(p, sl, st, ty, seg, (p.sizes[i] - 1) / 2, i);
+                mbar_arrive(&sm.v_empty[s]);
             }
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
             if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
             fuse_bar();
             const int gy = tc.y0 + ty;
             const bool row_ok = gy >= p.out_y0 && gy < p.out_y0 + p.out_rows;
+            const bool norm = M > 1 && p.blend_is_logits;
+            unsigned bad = 0;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
-                const float sc = (M > 1 && p.blend_is_logits) ? rcp_approx(st.S[j]) : 1.0f;
-                float o0 = st.a[j][0] * sc, o1 = st.a[j][1] * sc, o2 = st.a[j][2] * sc;
-                const int gx = tc.x0 + SEG * seg + j;
-                const bool bad = ((st.bad >> j) & 1u) || !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
-                if (bad && row_ok && gx < p.W && !(p.debug & 2)) {
-                    const float3 e = exact_pixel(p, tc.n, gx, gy);
-                    o0 = e.x;
-                    o1 = e.y;
-                    o2 = e.z;
-                }
+                const float sc = norm ? rcp_approx(st.S[j]) : 1.0f;
+                const float o0 = st.a[j][0] * sc, o1 = st.a[j][1] * sc, o2 = st.a[j][2] * sc;
+                const bool b = !(st.dmin[j] >= 1e-30f && st.dmax[j] <= 1e36f) ||
+                               !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
+                bad |= b ? (1u << j) : 0u;
                 sm.stage[0][ty][SEG * seg + j] = o0;
                 sm.stage[1][ty][SEG * seg + j] = o1;
                 sm.stage[2][ty][SEG * seg + j] = o2;
+            }
+            // rare: pixels outside the unshifted exp range -> exact evaluation
+            if (bad && row_ok && !(p.debug & 2)) {
+                for (int j = 0; j < SEG; ++j) {
+                    const int gx = tc.x0 + SEG * seg + j;
+                    if (((bad >> j) & 1u) && gx < p.W) {
+                        const float3 e = exact_pixel(p, tc.n, gx, gy);
+                        sm.stage[0][ty][SEG * seg + j] = e.x;
+                        sm.stage[1][ty][SEG * seg + j] = e.y;
+                        sm.stage[2][ty][SEG * seg + j] = e.z;
+                    }
+                }
             }
             fence_proxy_async();
             fuse_bar();
