@@ -49,6 +49,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* b, uns
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_spin(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "SPIN_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SPIN_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"

@@ -40,6 +40,10 @@
 namespace kmd {
 namespace tma {
 
+#ifdef KMD_SPIN_WAIT
+#define mbar_wait mbar_spin
+#endif
+
 constexpr int RMAX = 6;
 constexpr int TW = 52;              // output columns per tile
 constexpr int FW = TW + 2 * RMAX;   // 64 field columns (2 warps), global x0-6 .. x0+57
@@ -52,7 +56,8 @@ constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
 constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
 constexpr int VS = 68;
 constexpr int SEG = 13;             // pixels per fusion thread
-constexpr int NI = 5;               // input (importance) ring depth
+constexpr int NI = 4;               // input (importance) ring depth
+constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
 constexpr int NV = 3;               // V ring depth (field -> fusion)
 constexpr int NFIELD = 4;           // field warps
 constexpr int NFUSE = 3;            // fusion warps (TH * 4 segments = 96 threads)
@@ -66,6 +71,8 @@ struct InSlot {
 };
 struct Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
+};
+struct BSlot {
     alignas(128) float B[TH][BW];      // blend logits of map i, rows y0 .. y0+23, cols x0-8 .. x0+59
 };
 struct RadBuf {
@@ -75,10 +82,13 @@ struct Smem {
     RadBuf rad[2];
     InSlot in[NI];
     Slot slot[NV];
+    BSlot bl[NB];
     float stage[3][TH][TW];
-    unsigned long long rad_full[2], rad_empty[2], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV];
+    unsigned long long rad_full[2], rad_empty[2], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV], b_full[NB],
+        b_empty[NB];
 };
-static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlot) % 128 == 0,
+static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlot) % 128 == 0 &&
+                  sizeof(BSlot) % 128 == 0,
               "TMA destinations 128-B aligned");
 
 // ------------------------------------------------------------------ TMA PTX
@@ -210,35 +220,29 @@ __device__ __forceinline__ void field_job(Smem& sm, const InSlot& in, Slot& sl, 
 
 // --------------------------------------------------------------- fusion warps
 struct Acc {
-    float b0[SEG], S[SEG], a[SEG][3], dmin[SEG], dmax[SEG];
+    float S[SEG], a[SEG][3], dmin[SEG];
 };
 
 // Eq. 5 with alpha = softmax(B), accumulated one size
-// at a time.  The softmax is shifted by the first size's logit b0 (any shift
-// is exact, reading R2): a_i = exp(B_i - b0) with a_0 = 1, so S >= 1; an
-// overflow (B_i - b0 > 88) makes the pixel non-finite and sends it to the
-// exact path.  den range is tracked for the same check (reading R13).
-enum { FUSE_ONE = 0, FUSE_FIRST = 1, FUSE_LOGIT = 2, FUSE_ALPHA = 3 };
+// at a time.  The field warps have already replaced the blend logits B_i by
+// a_i = exp(B_i) (unshifted: any shift cancels in the softmax, reading R2),
+// so here  acc += a_i R_i,  S += a_i,  and Rhat = acc / S at the end.  A
+// logit beyond the fp32 exp range (S = 0 or inf, non-finite acc) or a tiny box
+// denominator sends the pixel to the exact path (reading R13).
+enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2 };
 
 template <int MODE>
-__device__ __forceinline__ void fuse_px(Acc& st, int j, float b, float4 v) {
-    const float den = v.x;
-    st.dmin[j] = fminf(st.dmin[j], den);
-    st.dmax[j] = fmaxf(st.dmax[j], den);
-    const float rden = rcp_approx(den);
+__device__ __forceinline__ void fuse_px(Acc& st, int j, float a, float4 v) {
+    st.dmin[j] = fminf(st.dmin[j], v.x);
+    const float rden = rcp_approx(v.x);
     float w;
     if constexpr (MODE == FUSE_ONE) {
         w = rden;
-    } else if constexpr (MODE == FUSE_FIRST) {  // a_0 = exp(B_0 - b0) = 1
-        st.b0[j] = b;
-        st.S[j] += 1.0f;
-        w = rden;
-    } else if constexpr (MODE == FUSE_LOGIT) {
-        const float a = exp_acc(b - st.b0[j]);
+    } else if constexpr (MODE == FUSE_SOFTMAX) {
         st.S[j] += a;
         w = a * rden;
     } else {  // alpha given (blend_is_logits == 0)
-        w = b * rden;
+        w = a * rden;
     }
     st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
     st.a[j][1] = fmaf(w, v.z, st.a[j][1]);
@@ -260,8 +264,8 @@ __device__ __forceinline__ void hbox(const Slot& sl, int ty, int seg, float4 (&o
     gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
 }
 
-__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, Acc& st, int ty, int seg, int R,
-                                         int i) {
+__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, const BSlot& bs, Acc& st, int ty,
+                                         int seg, int R, int i) {
     float4 o[SEG];
     switch (R) {
         case 0: hbox<0>(sl, ty, seg, o); break;
@@ -272,11 +276,10 @@ __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, A
         case 5: hbox<5>(sl, ty, seg, o); break;
         default: hbox<6>(sl, ty, seg, o); break;
     }
-    const float* Br = &sl.B[ty][SEG * seg + XOFF];
+    const float* Br = &bs.B[ty][SEG * seg + XOFF];
     if (p.M == 1) fuse_seg<FUSE_ONE>(st, Br, o);
     else if (!p.blend_is_logits) fuse_seg<FUSE_ALPHA>(st, Br, o);
-    else if (i == 0) fuse_seg<FUSE_FIRST>(st, Br, o);
-    else fuse_seg<FUSE_LOGIT>(st, Br, o);
+    else fuse_seg<FUSE_SOFTMAX>(st, Br, o);
 }
 
 // Exact per-pixel evaluation of Eq. 3-5 with per-window max shifts (R2), for
@@ -345,11 +348,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int s = 0; s < NI; ++s) {
             mbar_init(&sm.in_full[s], 1);
-            mbar_init(&sm.in_empty[s], 2 * 32);         // both halves, every lane
+            mbar_init(&sm.in_empty[s], 2);              // both halves (one elected lane each)
         }
         for (int s = 0; s < NV; ++s) {
-            mbar_init(&sm.v_full[s], 2 * 32 + 1);       // both halves + the blend expect_tx
-            mbar_init(&sm.v_empty[s], NFUSE * 32);
+            mbar_init(&sm.v_full[s], 2);                // both halves (one elected lane each)
+            mbar_init(&sm.v_empty[s], NFUSE);
+        }
+        for (int s = 0; s < NB; ++s) {
+            mbar_init(&sm.b_full[s], 1);
+            mbar_init(&sm.b_empty[s], NFUSE);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -363,37 +370,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
-            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4;
-            // Issue whichever load is ready first: the next tile's radiance
-            // (needs the field warps to be done with tile tl-1) or the next
-            // importance box (needs a free input slot).  Polling with test_wait
-            // keeps the importance ring full across tile boundaries.
-            int next_rad = 0, next_seq = 0;
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BW * 4;
+            // In-order, blocking issue (deadlock-free: every wait is on a step
+            // whose inputs were issued earlier).  The blend ring is primed here
+            // and refilled by the fusion warps as they release slots.
             const int total_seq = my_tiles * M;
-            while (next_rad < my_tiles || next_seq < total_seq) {
-                const bool rad_due = next_rad < my_tiles && next_rad <= next_seq / M + 1;
-                if (rad_due && mbar_test(&sm.rad_empty[next_rad & 1], ((next_rad >> 1) & 1) ^ 1)) {
-                    const Tile tc = tile_of(p, blockIdx.x + next_rad * gridDim.x, tiles_x, tiles_y);
-                    const int rb = next_rad & 1;
+            if (has_blend)
+                for (int q = 0; q < NB && q < total_seq; ++q) {
+                    const int tl = q / M, i = q - tl * M;
+                    const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                    mbar_arrive_expect_tx(&sm.b_full[q], B_BYTES);
+                    tma_load_3d(&sm.bl[q].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
+                                &sm.b_full[q]);
+                }
+            for (int tl = 0; tl < my_tiles; ++tl) {
+                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                const int rb = tl & 1;
+                mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1);
+                if (p.debug & 256) {
+                    mbar_arrive(&sm.rad_full[rb]);
+                } else {
                     mbar_arrive_expect_tx(&sm.rad_full[rb], RAD_BYTES);
                     tma_load_3d(&sm.rad[rb].v[0][0][0], &tm_rad, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base, tc.n * 3,
                                 &sm.rad_full[rb]);
-                    ++next_rad;
-                    continue;
                 }
-                if (next_seq < total_seq) {
-                    const int s = next_seq % NI;
-                    if (mbar_test(&sm.in_empty[s], ((next_seq / NI) & 1) ^ 1)) {
-                        const int tl = next_seq / M, i = next_seq - tl * M;
-                        const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                for (int i = 0; i < M; ++i) {
+                    const int seq = tl * M + i, s = seq % NI;
+                    mbar_wait(&sm.in_empty[s], ((seq / NI) & 1) ^ 1);
+                    if (p.debug & 128) {
+                        mbar_arrive(&sm.in_full[s]);
+                    } else {
                         mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES);
                         tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
                                     tc.n * M + i, &sm.in_full[s]);
-                        ++next_seq;
-                        continue;
                     }
                 }
-                __nanosleep(64);  // nothing ready: back off instead of stealing issue slots
             }
         }
     } else if (warp <= NFIELD) {
@@ -414,14 +425,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
                 Slot& sl = sm.slot[sv];
                 InSlot& in = sm.in[si];
-                mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);  // V slot (and its blend box) free
-                if (h == 0 && lane == 0) {
-                    mbar_arrive_expect_tx(&sm.v_full[sv], has_blend ? TH * BW * 4 : 0u);
-                    if (has_blend)
-                        tma_load_3d(&sl.B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
-                                    &sm.v_full[sv]);
-                }
+                mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);  // V slot free
                 mbar_wait(&sm.in_full[si], (seq / NI) & 1);
+                if (has_blend && p.blend_is_logits && !(p.debug & 64)) {
+                    // a_i = exp(B_i) for the output columns of this lane (reading
+                    // R2: the softmax shift cancels), in place in the blend box
+                    const int sb = seq % NB;
+                    mbar_wait(&sm.b_full[sb], (seq / NB) & 1);
+                    if (c >= RMAX && c < RMAX + TW) {
+                        float* bcol = &sm.bl[sb].B[0][c - RMAX + XOFF];
+#pragma unroll 4
+                        for (int r = 0; r < TH; ++r) bcol[r * BW] = exp_acc(bcol[r * BW]);
+                    }
+                }
                 if (border_rows && !(p.debug & 4)) {
                     fix_rows(&in.I[0][cc], FH * BW, 1, top, bot);
                     fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
@@ -436,8 +452,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     case 5: field_job<5>(sm, in, sl, rb, h, cc); break;
                     default: field_job<6>(sm, in, sl, rb, h, cc); break;
                 }
-                mbar_arrive(&sm.in_empty[si]);
-                mbar_arrive(&sm.v_full[sv]);
+                // one arrive per warp: __syncwarp orders every lane's shared
+                // memory accesses before the elected lane's release-arrive
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.in_empty[si]);
+                    mbar_arrive(&sm.v_full[sv]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.rad_empty[rb]);
@@ -451,19 +472,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             Acc st;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
-                st.b0[j] = 0.f;
                 st.S[j] = 0.f;
                 st.a[j][0] = st.a[j][1] = st.a[j][2] = 0.f;
                 st.dmin[j] = INFINITY;
-                st.dmax[j] = 0.f;
             }
             for (int i = 0; i < M; ++i) {
-                const int seq = tl * M + i, s = seq % NV;
+                const int seq = tl * M + i, s = seq % NV, sb = seq % NB;
                 mbar_wait(&sm.v_full[s], (seq / NV) & 1);
+                if (has_blend) mbar_wait(&sm.b_full[sb], (seq / NB) & 1);
                 const Slot& sl = sm.slot[s];
-                if (!(p.debug & 64)) fuse_job(p, sl, st, ty, seg, (p.sizes[i] - 1) / 2, i);
-                mbar_arrive(&sm.v_empty[s]);
+                if (!(p.debug & 64)) fuse_job(p, sl, sm.bl[sb], st, ty, seg, (p.sizes[i] - 1) / 2, i);
+                __syncwarp();
+                if ((c & 31) == 0) mbar_arrive(&sm.v_empty[s]);
+                if (has_blend) {
+                    if ((c & 31) == 0) mbar_arrive(&sm.b_empty[sb]);
+                    // refill this blend slot with step seq + NB once every fusion
+                    // thread has released it
+                    const int nq = seq + NB;
+                    if (c == 0 && nq < my_tiles * M) {
+                        mbar_wait(&sm.b_empty[sb], (seq / NB) & 1);
+                        const int ntl = nq / M, ni = nq - ntl * M;
+                        const Tile nt = tile_of(p, blockIdx.x + ntl * gridDim.x, tiles_x, tiles_y);
+                        mbar_arrive_expect_tx(&sm.b_full[sb], TH * BW * 4);
+                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, nt.x0 - XOFF, nt.y0 - p.out_y0, nt.n * M + ni,
+                                    &sm.b_full[sb]);
+                    }
+                }
             }
+            if (p.debug & 1024) continue;
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
             if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
             fuse_bar();
@@ -475,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < SEG; ++j) {
                 const float sc = norm ? rcp_approx(st.S[j]) : 1.0f;
                 const float o0 = st.a[j][0] * sc, o1 = st.a[j][1] * sc, o2 = st.a[j][2] * sc;
-                const bool b = !(st.dmin[j] >= 1e-30f && st.dmax[j] <= 1e36f) ||
+                const bool b = !(st.dmin[j] >= 1e-30f) || (norm && !(st.S[j] >= 1e-30f && st.S[j] <= 1e30f)) ||
                                !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
                 bad |= b ? (1u << j) : 0u;
                 sm.stage[0][ty][SEG * seg + j] = o0;
