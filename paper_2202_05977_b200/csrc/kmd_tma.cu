@@ -55,12 +55,13 @@ constexpr int FH = TH + 2 * RMAX;   // 36 field rows in every box
 constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
 constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
 constexpr int VS = 68;
-constexpr int SEG = 13;             // pixels per fusion thread
+constexpr int SEG = 7;              // pixels per fusion thread (segments of 7/6 alternate)
+constexpr int NSEG = 8;             // segments per output row: 52 = 4 x (7 + 6)
 constexpr int NI = 4;               // input (importance) ring depth
 constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
 constexpr int NV = 3;               // V ring depth (field -> fusion)
 constexpr int NFIELD = 4;           // field warps
-constexpr int NFUSE = 3;            // fusion warps (TH * 4 segments = 96 threads)
+constexpr int NFUSE = 6;            // fusion warps (TH * NSEG = 192 threads)
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 constexpr float L2E_LO = 1.925963033500011079e-08f;       // log2(e) - L2E
@@ -90,6 +91,20 @@ struct Smem {
 static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlot) % 128 == 0 &&
                   sizeof(BSlot) % 128 == 0,
               "TMA destinations 128-B aligned");
+
+// ---- optional timing instrumentation (build with -DKMD_INSTR; off in production)
+#ifdef KMD_INSTR
+constexpr int INSTR_TAGS = 16;
+__device__ unsigned long long g_instr[160 * 16 * INSTR_TAGS];
+#define IWAIT(tag, call)                                         \
+    do {                                                         \
+        const long long t0_ = clock64();                         \
+        call;                                                    \
+        instr[tag] += (unsigned long long)(clock64() - t0_);     \
+    } while (0)
+#else
+#define IWAIT(tag, call) call
+#endif
 
 // ------------------------------------------------------------------ TMA PTX
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
@@ -259,24 +274,24 @@ __device__ __forceinline__ void fuse_seg(Acc& st, const float* Br, const float4 
 // the radius: only this part differs between sizes, so the fusion code that
 // follows exists once -- keeps the fusion warps' hot code small).
 template <int R>
-__device__ __forceinline__ void hbox(const Slot& sl, int ty, int seg, float4 (&o)[SEG]) {
-    const float4* Vr = &sl.V[ty][SEG * seg + RMAX - R];
+__device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)[SEG]) {
+    const float4* Vr = &sl.V[ty][xs + RMAX - R];
     gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
 }
 
 __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, const BSlot& bs, Acc& st, int ty,
-                                         int seg, int R, int i) {
+                                         int xs, int R, int i) {
     float4 o[SEG];
     switch (R) {
-        case 0: hbox<0>(sl, ty, seg, o); break;
-        case 1: hbox<1>(sl, ty, seg, o); break;
-        case 2: hbox<2>(sl, ty, seg, o); break;
-        case 3: hbox<3>(sl, ty, seg, o); break;
-        case 4: hbox<4>(sl, ty, seg, o); break;
-        case 5: hbox<5>(sl, ty, seg, o); break;
-        default: hbox<6>(sl, ty, seg, o); break;
+        case 0: hbox<0>(sl, ty, xs, o); break;
+        case 1: hbox<1>(sl, ty, xs, o); break;
+        case 2: hbox<2>(sl, ty, xs, o); break;
+        case 3: hbox<3>(sl, ty, xs, o); break;
+        case 4: hbox<4>(sl, ty, xs, o); break;
+        case 5: hbox<5>(sl, ty, xs, o); break;
+        default: hbox<6>(sl, ty, xs, o); break;
     }
-    const float* Br = &bs.B[ty][SEG * seg + XOFF];
+    const float* Br = &bs.B[ty][xs + XOFF];
     if (p.M == 1) fuse_seg<FUSE_ONE>(st, Br, o);
     else if (!p.blend_is_logits) fuse_seg<FUSE_ALPHA>(st, Br, o);
     else fuse_seg<FUSE_SOFTMAX>(st, Br, o);
@@ -362,6 +377,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
     const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+#ifdef KMD_INSTR
+    unsigned long long instr[INSTR_TAGS] = {};
+    const long long t_begin = clock64();
+#endif
 
     if (warp == 0) {
         // ------------------------------------------------------------- TMA
@@ -386,7 +405,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tl = 0; tl < my_tiles; ++tl) {
                 const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
                 const int rb = tl & 1;
-                mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1);
+                IWAIT(0, mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1));
                 if (p.debug & 256) {
                     mbar_arrive(&sm.rad_full[rb]);
                 } else {
@@ -396,7 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 for (int i = 0; i < M; ++i) {
                     const int seq = tl * M + i, s = seq % NI;
-                    mbar_wait(&sm.in_empty[s], ((seq / NI) & 1) ^ 1);
+                    IWAIT(1, mbar_wait(&sm.in_empty[s], ((seq / NI) & 1) ^ 1));
                     if (p.debug & 128) {
                         mbar_arrive(&sm.in_full[s]);
                     } else {
@@ -417,7 +436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
             const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
             const bool border_rows = top > 0 || bot < FH;
-            mbar_wait(&sm.rad_full[rb], (tl >> 1) & 1);
+            IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl >> 1) & 1));
             for (int jl = fw; jl < 2 * M; jl += NFIELD) {
                 const int i = jl >> 1, h = jl & 1;
                 const int seq = tl * M + i, si = seq % NI, sv = seq % NV;
@@ -425,13 +444,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
                 Slot& sl = sm.slot[sv];
                 InSlot& in = sm.in[si];
-                mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);  // V slot free
-                mbar_wait(&sm.in_full[si], (seq / NI) & 1);
+                IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
+                IWAIT(4, mbar_wait(&sm.in_full[si], (seq / NI) & 1));
                 if (has_blend && p.blend_is_logits && !(p.debug & 64)) {
                     // a_i = exp(B_i) for the output columns of this lane (reading
                     // R2: the softmax shift cancels), in place in the blend box
                     const int sb = seq % NB;
-                    mbar_wait(&sm.b_full[sb], (seq / NB) & 1);
+                    IWAIT(5, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
                     if (c >= RMAX && c < RMAX + TW) {
                         float* bcol = &sm.bl[sb].B[0][c - RMAX + XOFF];
 #pragma unroll 4
@@ -466,7 +485,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
         // ----------------------------------------------------------- fusion
         const int c = threadIdx.x - (1 + NFIELD) * 32;
-        const int ty = c >> 2, seg = c & 3;
+        // thread = (row, segment); segments start at 0,7,13,20,26,33,39,46 and
+        // alternate 7/6 pixels; every thread computes 7 (the 7th of a 6-pixel
+        // segment is recomputed by its neighbour and not stored)
+        const int ty = c / NSEG, sub = c % NSEG;
+        const int xs = (sub * 13 + 1) >> 1, len = (sub & 1) ? SEG - 1 : SEG;
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             Acc st;
@@ -478,10 +501,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             for (int i = 0; i < M; ++i) {
                 const int seq = tl * M + i, s = seq % NV, sb = seq % NB;
-                mbar_wait(&sm.v_full[s], (seq / NV) & 1);
-                if (has_blend) mbar_wait(&sm.b_full[sb], (seq / NB) & 1);
+                IWAIT(6, mbar_wait(&sm.v_full[s], (seq / NV) & 1));
+                if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
                 const Slot& sl = sm.slot[s];
-                if (!(p.debug & 64)) fuse_job(p, sl, sm.bl[sb], st, ty, seg, (p.sizes[i] - 1) / 2, i);
+                if (!(p.debug & 64)) fuse_job(p, sl, sm.bl[sb], st, ty, xs, (p.sizes[i] - 1) / 2, i);
                 __syncwarp();
                 if ((c & 31) == 0) mbar_arrive(&sm.v_empty[s]);
                 if (has_blend) {
@@ -490,7 +513,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // thread has released it
                     const int nq = seq + NB;
                     if (c == 0 && nq < my_tiles * M) {
-                        mbar_wait(&sm.b_empty[sb], (seq / NB) & 1);
+                        IWAIT(8, mbar_wait(&sm.b_empty[sb], (seq / NB) & 1));
                         const int ntl = nq / M, ni = nq - ntl * M;
                         const Tile nt = tile_of(p, blockIdx.x + ntl * gridDim.x, tiles_x, tiles_y);
                         mbar_arrive_expect_tx(&sm.b_full[sb], TH * BW * 4);
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (p.debug & 1024) continue;
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
             if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
-            fuse_bar();
+            IWAIT(9, fuse_bar());
             const int gy = tc.y0 + ty;
             const bool row_ok = gy >= p.out_y0 && gy < p.out_y0 + p.out_rows;
             const bool norm = M > 1 && p.blend_is_logits;
@@ -514,24 +537,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const bool b = !(st.dmin[j] >= 1e-30f) || (norm && !(st.S[j] >= 1e-30f && st.S[j] <= 1e30f)) ||
                                !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
                 bad |= b ? (1u << j) : 0u;
-                sm.stage[0][ty][SEG * seg + j] = o0;
-                sm.stage[1][ty][SEG * seg + j] = o1;
-                sm.stage[2][ty][SEG * seg + j] = o2;
+                if (j < len) {
+                    sm.stage[0][ty][xs + j] = o0;
+                    sm.stage[1][ty][xs + j] = o1;
+                    sm.stage[2][ty][xs + j] = o2;
+                }
             }
             // rare: pixels outside the unshifted exp range -> exact evaluation
             if (bad && row_ok && !(p.debug & 2)) {
-                for (int j = 0; j < SEG; ++j) {
-                    const int gx = tc.x0 + SEG * seg + j;
+                for (int j = 0; j < len; ++j) {
+                    const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
                         const float3 e = exact_pixel(p, tc.n, gx, gy);
-                        sm.stage[0][ty][SEG * seg + j] = e.x;
-                        sm.stage[1][ty][SEG * seg + j] = e.y;
-                        sm.stage[2][ty][SEG * seg + j] = e.z;
+                        sm.stage[0][ty][xs + j] = e.x;
+                        sm.stage[1][ty][xs + j] = e.y;
+                        sm.stage[2][ty][xs + j] = e.z;
                     }
                 }
             }
             fence_proxy_async();
-            fuse_bar();
+            IWAIT(10, fuse_bar());
             if (tc.y0 >= p.out_y0) {
                 // TMA store; it clips the parts beyond W / out_rows.  (A TMA store
                 // with a negative coordinate faults on this B200, so the first tile
@@ -550,6 +575,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (c == 0) bulk_wait0();
     }
+#ifdef KMD_INSTR
+    instr[15] = (unsigned long long)(clock64() - t_begin);
+    if (lane == 0 && blockIdx.x < 160)
+        for (int t = 0; t < INSTR_TAGS; ++t) g_instr[(blockIdx.x * 16 + warp) * INSTR_TAGS + t] = instr[t];
+#endif
 }
 
 // ------------------------------------------------------------------- host
@@ -583,6 +613,12 @@ bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long plan
 }
 
 }  // namespace tma
+
+#ifdef KMD_INSTR
+extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, tma::g_instr, sizeof(unsigned long long) * n);
+}
+#endif
 
 bool tma_supported(const FusedParams& p) {
     if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % 4 != 0) return false;
