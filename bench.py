@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
+    ap.add_argument("--mode", choices=["frame", "band"], default="frame",
+                    help="frame: one frame per rank per step (weak scaling, default); band: ONE "
+                         "frame split into row bands across ranks with an NCCL halo exchange "
+                         "every step (strong scaling, BASELINE.json configs[3], default 4K)")
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--sizes", type=str, default=",".join(map(str, PAPER_SIZES)))
@@ -383,12 +387,78 @@ def run_kmd(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def run_band(args, rank, world, local):
+    """configs[3]: one 3840x2160 frame per step, split into `world` row bands.
+    Each step exchanges the r_max halo rows of the radiance and importance
+    planes with the neighbouring ranks (torch.distributed P2P = NCCL over
+    NVLink) and runs kmd_decode_filter_fuse_band on the rank's band."""
+    from paper_2202_05977_b200 import bands as B
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    sizes = [int(s) for s in args.sizes.split(",")]
+    H = args.height if args.height != 1080 else 2160
+    W = args.width if args.width != 1920 else 3840
+    M = len(sizes)
+    F = 2
+    K, Wm = args.steps, args.warmup
+    kmd.lib()
+    band = B.split_rows(H, world, sizes)[rank]
+    full = gen.make_inputs(F, H, W, M, device=dev)      # identical on every rank (same seeds)
+    rad = [B.slice_band(full.radiance[f:f + 1], band) for f in range(F)]
+    imp = [B.slice_band(full.importance[f:f + 1], band) for f in range(F)]
+    bl = [full.blend[f:f + 1, :, band.y0:band.y0 + band.rows].contiguous() for f in range(F)]
+    out = torch.empty((1, 3, band.rows, W), device=dev)
+    del full
+    torch.cuda.synchronize(dev)
+
+    def step(s):
+        f = s % F
+        if world > 1:
+            B.exchange_halos(rad[f], band, world)
+            B.exchange_halos(imp[f], band, world)
+        kmd.decode_filter_fuse_band(rad[f], imp[f], bl[f], sizes, y0=band.y0, band_rows=band.rows,
+                                    halo_top=band.halo_top, halo_bot=band.halo_bot, H_global=H,
+                                    out=out)
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        a.record()
+        for s in range(K):
+            step(s)
+        b.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    el = max_over_ranks(a.elapsed_time(b), world)
+    if rank != 0:
+        return
+    value = H * W * K / (el / 1e3) / 1e6
+    halo_bytes = 2 * 6 * W * (3 + M) * 4 if world > 1 else 0
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s (decode+filter+fusion, row bands)", "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": el / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{W}x{H} frame split into {world} row bands + NCCL halo exchange "
+                               f"(BASELINE.json configs[3])", "sizes": sizes,
+                   "band_rows": band.rows, "halo_bytes_per_seam": halo_bytes,
+                   "parallelism": f"row bands x{world}"},
+        "clocks": clk.summary(), "gpu_launches": K * kmd.launches_per_call(),
+        "timing": "CUDA events around K eager steps (exchange + band kernel), max over ranks"}),
+        flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup()
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.mode == "band":
+            run_band(args, rank, world, local)
         else:
             run_kmd(args, rank, world, local)
     finally:

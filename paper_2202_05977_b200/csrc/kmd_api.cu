@@ -185,11 +185,113 @@ kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* impor
     return run_fused(p, cfg, (cudaStream_t)stream);
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host entry point: each frame is cut into row bands; band b's rows (+ r_max
+// halo rows) are copied host->device with one 3-D copy per tensor, processed by
+// the band kernel and copied back, on three streams so the copy engines (H2D,
+// D2H) and the SMs overlap across bands and frames.  The caller's stream is
+// joined at the start and the end, so the call behaves as stream-ordered work.
+namespace {
+
+constexpr int HOST_MAX_BANDS = 4;
+
+struct HostBand {
+    int y0, rows, top, bot;  // owned rows [y0, y0+rows), halo rows above/below
+};
+
+int host_bands(int H, int rmax, HostBand* out) {
+    int nb = HOST_MAX_BANDS;
+    while (nb > 1 && H / nb < 2 * rmax + 8) --nb;
+    for (int b = 0; b < nb; ++b) {
+        const int y0 = (int)((int64_t)b * H / nb), y1 = (int)((int64_t)(b + 1) * H / nb);
+        out[b].y0 = y0;
+        out[b].rows = y1 - y0;
+        out[b].top = y0 < rmax ? y0 : rmax;
+        out[b].bot = H - y1 < rmax ? H - y1 : rmax;
+    }
+    return nb;
+}
+
+// floats of one frame's band buffers: radiance + importance with halos, blend + out without
+size_t host_frame_floats(int H, int W, int M, int rmax) {
+    HostBand bb[HOST_MAX_BANDS];
+    const int nb = host_bands(H, rmax, bb);
+    size_t f = 0;
+    for (int b = 0; b < nb; ++b) {
+        const size_t buf = (size_t)(bb[b].top + bb[b].rows + bb[b].bot) * W;
+        f += buf * (3 + M) + (size_t)bb[b].rows * W * (M + 3);
+        f = (f + 31) & ~(size_t)31;  // keep every band 128-byte aligned
+    }
+    return f;
+}
+
+struct HostStreams {
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t join = nullptr, done = nullptr;
+    cudaEvent_t in[2][HOST_MAX_BANDS] = {}, kern[2][HOST_MAX_BANDS] = {}, out[2][HOST_MAX_BANDS] = {};
+    bool ok = false;
+    int dev = -1;
+};
+thread_local HostStreams g_hs;
+
+cudaError_t host_streams(HostStreams** hs) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!g_hs.ok || g_hs.dev != dev) {
+        HostStreams h;
+        const unsigned fl = cudaStreamNonBlocking;
+        if ((e = cudaStreamCreateWithFlags(&h.h2d, fl)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&h.comp, fl)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&h.d2h, fl)) != cudaSuccess) return e;
+        const unsigned ef = cudaEventDisableTiming;
+        if ((e = cudaEventCreateWithFlags(&h.join, ef)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&h.done, ef)) != cudaSuccess) return e;
+        for (int s = 0; s < 2; ++s)
+            for (int b = 0; b < HOST_MAX_BANDS; ++b) {
+                if ((e = cudaEventCreateWithFlags(&h.in[s][b], ef)) != cudaSuccess) return e;
+                if ((e = cudaEventCreateWithFlags(&h.kern[s][b], ef)) != cudaSuccess) return e;
+                if ((e = cudaEventCreateWithFlags(&h.out[s][b], ef)) != cudaSuccess) return e;
+            }
+        h.ok = true;
+        h.dev = dev;
+        g_hs = h;  // (streams of a previous device are left to the driver at exit)
+    }
+    *hs = &g_hs;
+    return cudaSuccess;
+}
+
+// rows [r0, r0+nr) of `planes` planes of an [planes][H][W] host tensor <-> a
+// dense [planes][nr][W] device buffer, one 3-D copy
+cudaError_t copy_rows(void* dev, const void* host, int W, int H, int planes, int r0, int nr, bool to_dev,
+                      cudaStream_t st) {
+    cudaMemcpy3DParms c = {};
+    const size_t pitch = (size_t)W * sizeof(float);
+    cudaPitchedPtr hp = make_cudaPitchedPtr((void*)((const float*)host + (size_t)r0 * W), pitch, W, H);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dev, pitch, W, nr);
+    if (to_dev) {
+        c.srcPtr = hp;
+        c.dstPtr = dp;
+        c.kind = cudaMemcpyHostToDevice;
+    } else {
+        c.srcPtr = dp;
+        c.dstPtr = hp;
+        c.kind = cudaMemcpyDeviceToHost;
+    }
+    c.extent = make_cudaExtent(pitch, nr, planes);
+    return cudaMemcpy3DAsync(&c, st);
+}
+
+}  // namespace
+
+extern "C" {
+
 size_t kmd_host_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg) {
     if (!cfg || N < 1 || H < 1 || W < 1 || cfg->num_sizes < 1 || cfg->num_sizes > KMD_MAX_SIZES) return 0;
-    // one frame of inputs + output, double-buffered when N > 1
-    const size_t frame = (size_t)H * W * sizeof(float) * (size_t)(3 + 2 * cfg->num_sizes + 3);
-    return frame * (N > 1 ? 2 : 1);
+    const size_t frame = host_frame_floats(H, W, cfg->num_sizes, rmax_of(cfg)) * sizeof(float);
+    return frame * (N > 1 ? 2 : 1);  // two frames in flight when N > 1
 }
 
 kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
@@ -212,35 +314,59 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     const size_t need = kmd_host_workspace_bytes(N, H, W, cfg);
     if (workspace_bytes < need)
         return fail(KMD_ERR_DIM, "workspace %zu bytes < required %zu", workspace_bytes, need);
-    const int M = cfg->num_sizes;
+    HostStreams* hs = nullptr;
+    cudaError_t e = host_streams(&hs);
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams");
+    const int M = cfg->num_sizes, rmax = rmax_of(cfg);
     const size_t plane = (size_t)H * W;
-    const size_t frame_floats = plane * (size_t)(3 + 2 * M + 3);
-    cudaStream_t st = (cudaStream_t)stream;
+    const size_t frame_floats = host_frame_floats(H, W, M, rmax);
+    HostBand bb[HOST_MAX_BANDS];
+    const int nb = host_bands(H, rmax, bb);
+    cudaStream_t user = (cudaStream_t)stream;
+    // everything already queued on the caller's stream happens first
+    if ((e = cudaEventRecord(hs->join, user)) != cudaSuccess) return cuda_fail(e, "event record");
+    for (cudaStream_t st : {hs->h2d, hs->comp, hs->d2h})
+        if ((e = cudaStreamWaitEvent(st, hs->join, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     for (int n = 0; n < N; ++n) {
-        float* base = (float*)device_workspace + (size_t)(n & (N > 1 ? 1 : 0)) * frame_floats;
-        float* d_rad = base;
-        float* d_imp = d_rad + 3 * plane;
-        float* d_blend = d_imp + M * plane;
-        float* d_out = d_blend + M * plane;
-        cudaError_t e;
-        e = cudaMemcpyAsync(d_rad, radiance_host + (size_t)n * 3 * plane, 3 * plane * sizeof(float),
-                            cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D radiance");
-        e = cudaMemcpyAsync(d_imp, importance_host + (size_t)n * M * plane, M * plane * sizeof(float),
-                            cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D importance");
-        if (M > 1) {
-            e = cudaMemcpyAsync(d_blend, blend_host + (size_t)n * M * plane, M * plane * sizeof(float),
-                                cudaMemcpyHostToDevice, st);
-            if (e != cudaSuccess) return cuda_fail(e, "H2D blend");
+        const int set = n & 1;
+        float* base = (float*)device_workspace + (size_t)(N > 1 ? set : 0) * frame_floats;
+        const float* rh = radiance_host + (size_t)n * 3 * plane;
+        const float* ih = importance_host + (size_t)n * M * plane;
+        const float* bh = M > 1 ? blend_host + (size_t)n * M * plane : nullptr;
+        float* oh = out_host + (size_t)n * 3 * plane;
+        float* cur = base;
+        for (int b = 0; b < nb; ++b) {
+            const HostBand& B = bb[b];
+            const int buf_rows = B.top + B.rows + B.bot;
+            float* d_rad = cur;
+            float* d_imp = d_rad + (size_t)3 * buf_rows * W;
+            float* d_bl = d_imp + (size_t)M * buf_rows * W;
+            float* d_out = d_bl + (size_t)M * B.rows * W;
+            cur = d_out + (size_t)3 * B.rows * W;
+            cur = base + ((size_t)(cur - base) + 31 & ~(size_t)31);
+            // the buffers of this set were last used two frames ago: wait for that D2H
+            if (n >= 2 && (e = cudaStreamWaitEvent(hs->h2d, hs->out[set][b], 0)) != cudaSuccess)
+                return cuda_fail(e, "stream wait");
+            const int r0 = B.y0 - B.top;
+            if ((e = copy_rows(d_rad, rh, W, H, 3, r0, buf_rows, true, hs->h2d)) != cudaSuccess ||
+                (e = copy_rows(d_imp, ih, W, H, M, r0, buf_rows, true, hs->h2d)) != cudaSuccess ||
+                (bh && (e = copy_rows(d_bl, bh, W, H, M, B.y0, B.rows, true, hs->h2d)) != cudaSuccess))
+                return cuda_fail(e, "H2D band copy");
+            if ((e = cudaEventRecord(hs->in[set][b], hs->h2d)) != cudaSuccess) return cuda_fail(e, "event record");
+            if ((e = cudaStreamWaitEvent(hs->comp, hs->in[set][b], 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+            kmd_status s = kmd_decode_filter_fuse_band(d_rad, d_imp, bh ? d_bl : nullptr, d_out, 1, B.rows, W,
+                                                       B.top, B.bot, B.y0, H, cfg, hs->comp);
+            if (s) return s;
+            if ((e = cudaEventRecord(hs->kern[set][b], hs->comp)) != cudaSuccess) return cuda_fail(e, "event record");
+            if ((e = cudaStreamWaitEvent(hs->d2h, hs->kern[set][b], 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+            if ((e = copy_rows(d_out, oh, W, H, 3, B.y0, B.rows, false, hs->d2h)) != cudaSuccess)
+                return cuda_fail(e, "D2H band copy");
+            if ((e = cudaEventRecord(hs->out[set][b], hs->d2h)) != cudaSuccess) return cuda_fail(e, "event record");
         }
-        kmd_status s = kmd_decode_filter_fuse(d_rad, d_imp, M > 1 ? d_blend : nullptr, d_out, 1, H, W,
-                                              cfg, stream);
-        if (s) return s;
-        e = cudaMemcpyAsync(out_host + (size_t)n * 3 * plane, d_out, 3 * plane * sizeof(float),
-                            cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H out");
     }
+    // the caller's stream resumes after the last band's D2H (d2h is in order)
+    if ((e = cudaEventRecord(hs->done, hs->d2h)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(user, hs->done, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     return KMD_OK;
 }
 
