@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--sizes", type=str, default=",".join(map(str, PAPER_SIZES)))
     ap.add_argument("--rotate", type=int, default=4, help="distinct resident frames per rank")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--albedo", action="store_true",
+                    help="NEXT row 1: fuse the albedo remodulation epilogue (out = Rhat * albedo)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU seconds for the oracle sample")
@@ -245,15 +247,17 @@ def run_kmd(args, rank, world, local):
     # resident inputs: F distinct frames per rank (frame ids rank*F .. rank*F+F-1)
     inp = gen.make_inputs(F, H, W, M, frame_offset=rank * F, device=dev)
     outs = torch.empty((F, 3, H, W), device=dev)
+    alb = gen.make_albedo(F, H, W, frame_offset=rank * F, device=dev) if args.albedo else None
     views = [(inp.radiance[f:f + 1], inp.importance[f:f + 1],
-              None if inp.blend is None else inp.blend[f:f + 1], outs[f:f + 1])
+              None if inp.blend is None else inp.blend[f:f + 1], outs[f:f + 1],
+              None if alb is None else alb[f:f + 1])
              for f in range(F)]
     stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize(dev)
 
     def step(s, strm=None):
-        r, i, b, o = views[s % F]
-        kmd.decode_filter_fuse(r, i, b, sizes, out=o, stream=strm)
+        r, i, b, o, a = views[s % F]
+        kmd.decode_filter_fuse(r, i, b, sizes, out=o, stream=strm, albedo=a)
 
     for s in range(Wm):
         step(s, stream)
@@ -305,10 +309,12 @@ def run_kmd(args, rank, world, local):
 
     px_per_step = H * W * world
     value = px_per_step * K / (el_ms_max / 1e3) / 1e6
-    bytes_launch = kmd.algorithmic_bytes(1, H, W, sizes, inp.blend is not None)
+    bytes_launch = kmd.algorithmic_bytes(1, H, W, sizes, inp.blend is not None) + \
+        (12 * H * W if args.albedo else 0)
     achieved = bytes_launch / (kern_avg_ms / 1e3) / 1e9
     peak, peak_src = measured_peak_hbm()
-    workload = f"{W}x{H} frame, sizes {sizes}, fusion (BASELINE.json configs[2])"
+    workload = f"{W}x{H} frame, sizes {sizes}, fusion (BASELINE.json configs[2])" + \
+        (" + albedo remodulation (NEXT row 1)" if args.albedo else "")
 
     # ---- e2e: through the C ABI with pinned HOST buffers ---------------------
     e2e = None
@@ -350,7 +356,7 @@ def run_kmd(args, rank, world, local):
                "kind": "oracle",
                "sample": f"rows {y0}..{y0 + rows} ({rows * W} px) of frame 0 of the {W}x{H} "
                          f"M={M} workload, fp64 oracle, {dt:.1f} s"}
-        r0, i0, b0, o0 = views[0]
+        r0, i0, b0, o0, a0 = views[0]
         kmd.decode_filter_fuse(r0, i0, b0, sizes, out=o0, stream=stream)
         torch.cuda.synchronize(dev)
         got = outs[0:1, :, y0:y0 + rows].cpu().numpy().astype(np.float64)

@@ -95,6 +95,26 @@ kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance
                                   const float* blend, float* out, int32_t N, int32_t H,
                                   int32_t W, const kmd_config* cfg, kmd_stream_t stream);
 
+/* Hot path + remodulation epilogue (NEXT row 1; Fig. 1, 258: "we
+ * filter the noisy input irradiance without albedo, and at the last step, we
+ * multiply back the albedo"): out = Rhat * albedo, in the same pass.
+ *   albedo [N,3,H,W] device (NULL = plain kmd_decode_filter_fuse); other
+ *   arguments, errors and numerics as kmd_decode_filter_fuse.               */
+kmd_status kmd_decode_filter_fuse_remod(const float* radiance, const float* importance,
+                                        const float* blend, const float* albedo, float* out,
+                                        int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                                        kmd_stream_t stream);
+
+/* Albedo demodulation before filtering:
+ * irradiance = radiance / max(albedo, eps), elementwise over [N,3,H,W] device
+ * buffers; eps > 0 (else KMD_ERR_CONFIG); irradiance may alias radiance.     */
+kmd_status kmd_demodulate(const float* radiance, const float* albedo, float eps, float* irradiance,
+                          int32_t N, int32_t H, int32_t W, kmd_stream_t stream);
+
+/* Remodulation on its own: out = irradiance * albedo. */
+kmd_status kmd_remodulate(const float* irradiance, const float* albedo, float* out, int32_t N,
+                          int32_t H, int32_t W, kmd_stream_t stream);
+
 /* One size, no fusion: out_i = R^{k}(p,c) of Eq. 3-4.
  *   radiance [N,3,H,W], importance_i [N,1,H,W], out_i [N,3,H,W], all device.   */
 kmd_status kmd_decode_filter(const float* radiance, const float* importance_i, float* out_i,

@@ -63,9 +63,11 @@ def _load():
         lib.kmdo_decode_filter_fuse_pixels.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
                                                        P, P, P, ctypes.c_int64, i32, P]
         lib.kmdo_max_threads.argtypes = []
+        lib.kmdo_demodulate.argtypes = [P, P, ctypes.c_double, ctypes.c_int64, P]
+        lib.kmdo_remodulate.argtypes = [P, P, ctypes.c_int64, P]
         for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
                   "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
-                  "kmdo_max_threads"):
+                  "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -181,4 +183,25 @@ def decode_filter_fuse_pixels(radiance, importance, blend, sizes: Sequence[int],
     _check(_load().kmdo_decode_filter_fuse_pixels(
         _ptr(radiance), _ptr(importance), _ptr(b), N, H, W, M, _ptr(sz),
         int(bool(blend_is_logits)), _ptr(n), _ptr(y), _ptr(x), len(n), threads, _ptr(out)))
+    return out
+
+
+# ------------------------------------------------------ albedo (NEXT row 1)
+def demodulate(radiance, albedo, eps: float = 1e-3) -> np.ndarray:
+    """SPEC.md:127-136: irradiance = radiance / max(albedo, eps) (fp64)."""
+    r = _f32(radiance)
+    a = _f32(albedo)
+    assert r.shape == a.shape
+    out = np.empty(r.shape, dtype=np.float64)
+    _check(_load().kmdo_demodulate(_ptr(r), _ptr(a), float(eps), r.size, _ptr(out)))
+    return out
+
+
+def remodulate(irradiance, albedo) -> np.ndarray:
+    """SPEC.md:138-145 / PAPER.md:181: out = irradiance * albedo (fp64)."""
+    x = np.ascontiguousarray(irradiance, dtype=np.float64)
+    a = _f32(albedo)
+    assert x.shape == a.shape
+    out = np.empty(x.shape, dtype=np.float64)
+    _check(_load().kmdo_remodulate(_ptr(x), _ptr(a), x.size, _ptr(out)))
     return out

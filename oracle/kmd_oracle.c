@@ -315,6 +315,23 @@ int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importanc
     return err;
 }
 
+/* ---- albedo demodulation / remodulation */
+int kmdo_demodulate(const float* radiance, const float* albedo, double eps, int64_t count, double* out) {
+    if (!radiance || !albedo || !out) return KMDO_ERR_NULL;
+    if (!(eps > 0.0)) return KMDO_ERR_CONFIG;
+    for (int64_t t = 0; t < count; ++t) {
+        const double a = (double)albedo[t];
+        out[t] = (double)radiance[t] / (a > eps ? a : eps);
+    }
+    return KMDO_OK;
+}
+
+int kmdo_remodulate(const double* irradiance, const float* albedo, int64_t count, double* out) {
+    if (!irradiance || !albedo || !out) return KMDO_ERR_NULL;
+    for (int64_t t = 0; t < count; ++t) out[t] = irradiance[t] * (double)albedo[t];
+    return KMDO_OK;
+}
+
 int kmdo_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -83,6 +83,14 @@ int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importanc
                                    const int32_t* n, const int32_t* y, const int32_t* x,
                                    int64_t count, int32_t threads, double* out);
 
+/* Albedo demodulation ("filter the noisy input
+ * irradiance without albedo"): out[t] = radiance[t] / max(albedo[t], eps). */
+int kmdo_demodulate(const float* radiance, const float* albedo, double eps, int64_t count, double* out);
+
+/* Remodulation (Fig. 1 "multiply back the
+ * albedo"): out[t] = irradiance[t] * albedo[t]. */
+int kmdo_remodulate(const double* irradiance, const float* albedo, int64_t count, double* out);
+
 /* Threads OpenMP would use for threads <= 0 (reported as cpu_baseline.cores). */
 int kmdo_max_threads(void);
 

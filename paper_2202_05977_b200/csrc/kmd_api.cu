@@ -85,9 +85,10 @@ kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t str
 
 extern "C" {
 
-kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance,
-                                  const float* blend, float* out, int32_t N, int32_t H,
-                                  int32_t W, const kmd_config* cfg, kmd_stream_t stream) {
+kmd_status kmd_decode_filter_fuse_remod(const float* radiance, const float* importance,
+                                        const float* blend, const float* albedo, float* out,
+                                        int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                                        kmd_stream_t stream) {
     g_err[0] = 0;
     if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
     if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
@@ -103,13 +104,47 @@ kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance
     const size_t M = (size_t)cfg->num_sizes;
     if (overlaps(out, 3 * N * plane, radiance, 3 * N * plane) ||
         overlaps(out, 3 * N * plane, importance, M * N * plane) ||
-        (M > 1 && overlaps(out, 3 * N * plane, blend, M * N * plane)))
+        (M > 1 && overlaps(out, 3 * N * plane, blend, M * N * plane)) ||
+        overlaps(out, 3 * N * plane, albedo, 3 * N * plane))
         return fail(KMD_ERR_ALIAS, "out overlaps an input");
     kmd::FusedParams p{};
-    p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out;
+    p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out; p.albedo = albedo;
     p.N = N; p.W = W; p.H = H;
     p.row_base = 0; p.buf_rows = H; p.out_y0 = 0; p.out_rows = H;
     return run_fused(p, cfg, (cudaStream_t)stream);
+}
+
+kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance,
+                                  const float* blend, float* out, int32_t N, int32_t H,
+                                  int32_t W, const kmd_config* cfg, kmd_stream_t stream) {
+    return kmd_decode_filter_fuse_remod(radiance, importance, blend, nullptr, out, N, H, W, cfg, stream);
+}
+
+kmd_status kmd_demodulate(const float* radiance, const float* albedo, float eps, float* irradiance,
+                          int32_t N, int32_t H, int32_t W, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0 || (N > 0 && (H < 1 || W < 1))) return fail(KMD_ERR_DIM, "bad N/H/W");
+    if (!(eps > 0.f)) return fail(KMD_ERR_CONFIG, "eps must be > 0");
+    if (N == 0) return KMD_OK;
+    if (!radiance || !albedo || !irradiance) return fail(KMD_ERR_NULL, "NULL buffer");
+    const size_t bytes = (size_t)N * 3 * H * W * sizeof(float);
+    if (overlaps(irradiance, bytes, albedo, bytes)) return fail(KMD_ERR_ALIAS, "irradiance overlaps albedo");
+    cudaError_t e = kmd::launch_albedo_op(radiance, albedo, eps, irradiance, (long long)N * 3 * H * W, 0,
+                                          (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "demodulate launch");
+}
+
+kmd_status kmd_remodulate(const float* irradiance, const float* albedo, float* out, int32_t N, int32_t H,
+                          int32_t W, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0 || (N > 0 && (H < 1 || W < 1))) return fail(KMD_ERR_DIM, "bad N/H/W");
+    if (N == 0) return KMD_OK;
+    if (!irradiance || !albedo || !out) return fail(KMD_ERR_NULL, "NULL buffer");
+    const size_t bytes = (size_t)N * 3 * H * W * sizeof(float);
+    if (overlaps(out, bytes, albedo, bytes)) return fail(KMD_ERR_ALIAS, "out overlaps albedo");
+    cudaError_t e = kmd::launch_albedo_op(irradiance, albedo, 0.f, out, (long long)N * 3 * H * W, 1,
+                                          (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "remodulate launch");
 }
 
 kmd_status kmd_decode_filter(const float* radiance, const float* importance_i, float* out_i,

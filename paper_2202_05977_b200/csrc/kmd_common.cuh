@@ -17,6 +17,7 @@ struct FusedParams {
     const float* imp;    // [N,M,buf_rows,W]
     const float* blend;  // [N,M,out_rows,W] or nullptr (M == 1)
     float* out;          // [N,3,out_rows,W]
+    const float* albedo; // [N,3,out_rows,W] or nullptr: out = Rhat * albedo (remodulation epilogue)
     int N, W, H;         // H = rows of the whole frame (clamp bound)
     int row_base;        // global row held by buffer row 0 of rad/imp
     int buf_rows;        // rows held by rad/imp
@@ -31,6 +32,18 @@ struct FusedParams {
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// Remodulation epilogue (Fig. 1, 258: "multiply back the albedo"):
+// scales the fused value of output pixel (n, global row gy, column gx) in place.
+__device__ __forceinline__ void remodulate(const FusedParams& p, int n, int gy, int gx, float& o0, float& o1,
+                                           float& o2) {
+    if (!p.albedo) return;
+    const size_t oplane = (size_t)p.out_rows * p.W;
+    const float* a = p.albedo + (size_t)n * 3 * oplane + (size_t)(gy - p.out_y0) * p.W + gx;
+    o0 *= __ldg(a);
+    o1 *= __ldg(a + oplane);
+    o2 *= __ldg(a + 2 * oplane);
+}
 
 // ---- sm_90+/sm_100a primitives shared by the pipelined kernels -------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

@@ -176,9 +176,11 @@ __global__ void __launch_bounds__(NT) fused_direct_kernel(FusedParams p) {
         const int gy = y0 + ty, gx = x0 + tx;
         if (gx < p.W && gy >= p.out_y0 && gy < p.out_y0 + p.out_rows) {
             const size_t o = (size_t)(gy - p.out_y0) * p.W + gx;
-            out[o] = acc[j][0];
-            out[oplane + o] = acc[j][1];
-            out[2 * oplane + o] = acc[j][2];
+            float o0 = acc[j][0], o1 = acc[j][1], o2 = acc[j][2];
+            remodulate(p, n, gy, gx, o0, o1, o2);
+            out[o] = o0;
+            out[oplane + o] = o1;
+            out[2 * oplane + o] = o2;
         }
     }
 }

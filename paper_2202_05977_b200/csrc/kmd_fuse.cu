@@ -44,7 +44,30 @@ __global__ void __launch_bounds__(256) fuse_kernel(const float* __restrict__ fil
     }
 }
 
+// irradiance = radiance / max(albedo, eps);
+// remodulation multiplies back.  Elementwise, HBM-bound, float4 when aligned.
+__global__ void __launch_bounds__(256) albedo_kernel(const float* __restrict__ x, const float* __restrict__ a,
+                                                     float eps, float* __restrict__ out, long long n, int op) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const float v = __ldg(x + t), al = __ldg(a + t);
+        out[t] = op == 0 ? v / fmaxf(al, eps) : v * al;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_albedo_op(const float* x, const float* albedo, float eps, float* out, long long n, int op,
+                             cudaStream_t stream) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long blocks = (n + 255) / 256;
+    if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
+    if (blocks < 1) blocks = 1;
+    albedo_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, albedo, eps, out, n, op);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
                              int H, int W, int M, int blend_is_logits, cudaStream_t stream) {

@@ -19,4 +19,8 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream);
 cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
                              int H, int W, int M, int blend_is_logits, cudaStream_t stream);
 
+// albedo demodulation (op 0: x / max(albedo, eps)) and remodulation (op 1: x * albedo), kmd_fuse.cu
+cudaError_t launch_albedo_op(const float* x, const float* albedo, float eps, float* out, long long n, int op,
+                             cudaStream_t stream);
+
 }  // namespace kmd

@@ -492,6 +492,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int xs = (sub * 13 + 1) >> 1, len = (sub & 1) ? SEG - 1 : SEG;
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            // albedo of this thread's pixels, loaded now so the latency hides
+            // behind the M sizes (remodulation epilogue)
+            float alb[SEG][3];
+            if (p.albedo) {
+                const size_t op = (size_t)p.out_rows * p.W;
+                const int gyc = clampi(tc.y0 + ty - p.out_y0, 0, p.out_rows - 1);
+                const float* ab = p.albedo + (size_t)tc.n * 3 * op + (size_t)gyc * p.W;
+#pragma unroll
+                for (int j = 0; j < SEG; ++j) {
+                    const int gxc = min(tc.x0 + xs + j, p.W - 1);
+                    alb[j][0] = __ldg(ab + gxc);
+                    alb[j][1] = __ldg(ab + op + gxc);
+                    alb[j][2] = __ldg(ab + 2 * op + gxc);
+                }
+            }
             Acc st;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
@@ -538,9 +553,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
                 bad |= b ? (1u << j) : 0u;
                 if (j < len) {
-                    sm.stage[0][ty][xs + j] = o0;
-                    sm.stage[1][ty][xs + j] = o1;
-                    sm.stage[2][ty][xs + j] = o2;
+                    float r0 = o0, r1 = o1, r2 = o2;
+                    const int gx = tc.x0 + xs + j;
+                    if (p.albedo) {
+                        r0 *= alb[j][0];
+                        r1 *= alb[j][1];
+                        r2 *= alb[j][2];
+                    }
+                    sm.stage[0][ty][xs + j] = r0;
+                    sm.stage[1][ty][xs + j] = r1;
+                    sm.stage[2][ty][xs + j] = r2;
                 }
             }
             // rare: pixels outside the unshifted exp range -> exact evaluation
@@ -548,7 +570,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int j = 0; j < len; ++j) {
                     const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
-                        const float3 e = exact_pixel(p, tc.n, gx, gy);
+                        float3 e = exact_pixel(p, tc.n, gx, gy);
+                        remodulate(p, tc.n, gy, gx, e.x, e.y, e.z);
                         sm.stage[0][ty][xs + j] = e.x;
                         sm.stage[1][ty][xs + j] = e.y;
                         sm.stage[2][ty][xs + j] = e.z;
@@ -624,7 +647,7 @@ bool tma_supported(const FusedParams& p) {
     if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % 4 != 0) return false;
     for (int i = 0; i < p.M; ++i)
         if ((p.sizes[i] - 1) / 2 > tma::RMAX) return false;
-    const uintptr_t a = (uintptr_t)p.rad | (uintptr_t)p.imp | (uintptr_t)p.out | (uintptr_t)p.blend;
+    const uintptr_t a = (uintptr_t)p.rad | (uintptr_t)p.imp | (uintptr_t)p.out | (uintptr_t)p.blend;  // albedo: LDG
     if (a & 15) return false;
     return tma::get_encode() != nullptr;
 }

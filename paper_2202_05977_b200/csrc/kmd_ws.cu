@@ -329,8 +329,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_ws_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
                 const float sc = (M > 1 && p.blend_is_logits) ? rcp_approx(st.S[j]) : 1.0f;
-#pragma unroll
-                for (int ch = 0; ch < 3; ++ch) sm.stage[ch][ty][SEG * seg + j] = st.acc[j][ch] * sc;
+                float o0 = st.acc[j][0] * sc, o1 = st.acc[j][1] * sc, o2 = st.acc[j][2] * sc;
+                const int gx = tc.x0 + SEG * seg + j, gy = tc.y0 + ty;
+                if (gx < p.W && gy >= p.out_y0 && gy < p.out_y0 + p.out_rows) remodulate(p, tc.n, gy, gx, o0, o1, o2);
+                sm.stage[0][ty][SEG * seg + j] = o0;
+                sm.stage[1][ty][SEG * seg + j] = o1;
+                sm.stage[2][ty][SEG * seg + j] = o2;
             }
             consumer_bar();
             float* out = p.out + (size_t)tc.n * 3 * oplane;

@@ -105,3 +105,18 @@ def make_inputs(N: int, H: int, W: int, M: int, seed: int = BASE_SEED, frame_off
 def sizes_from(k_b: int = 3, k_s: int = 2, M: int = 6) -> Sequence[int]:
     """k_i = k_b + i * k_s (PAPER.md:324; SPEC.md:228-231)."""
     return tuple(k_b + i * k_s for i in range(M))
+
+
+def make_albedo(N: int, H: int, W: int, seed: int = BASE_SEED + 7, frame_offset: int = 0,
+                device="cpu") -> torch.Tensor:
+    """Albedo [N,3,H,W] in (0, 1): a smooth texture (0.05..0.95) with 1% texels
+    forced to 0 (the demodulation eps floor)."""
+    device = torch.device(device)
+    out = []
+    for f in range(N):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed + frame_offset + f)
+        a = 0.05 + 0.9 * torch.sigmoid(1.5 * _smooth(g, 3, H, W, device))
+        zero = torch.rand((1, H, W), generator=g, device=device) < 0.01
+        out.append(torch.where(zero, torch.zeros_like(a), a))
+    return torch.stack(out).contiguous()

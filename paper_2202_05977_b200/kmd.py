@@ -51,7 +51,8 @@ def make_config(sizes: Sequence[int], blend_is_logits: bool = True) -> kmd_confi
 
 _lib = None
 
-EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter", "kmd_fuse",
+EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
+           "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
            "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
            "kmd_status_string", "kmd_last_error", "kmd_version")
@@ -70,6 +71,9 @@ def lib(build_if_missing: bool = True):
     P, i32 = ctypes.c_void_p, ctypes.c_int32
     C = ctypes.POINTER(kmd_config)
     L.kmd_decode_filter_fuse.argtypes = [P, P, P, P, i32, i32, i32, C, P]
+    L.kmd_decode_filter_fuse_remod.argtypes = [P, P, P, P, P, i32, i32, i32, C, P]
+    L.kmd_demodulate.argtypes = [P, P, ctypes.c_float, P, i32, i32, i32, P]
+    L.kmd_remodulate.argtypes = [P, P, P, i32, i32, i32, P]
     L.kmd_decode_filter.argtypes = [P, P, P, i32, i32, i32, i32, P]
     L.kmd_fuse.argtypes = [P, P, P, i32, i32, i32, i32, i32, P]
     L.kmd_decode_filter_fuse_band.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, P]
@@ -84,7 +88,8 @@ def lib(build_if_missing: bool = True):
     L.kmd_last_error.argtypes = []
     L.kmd_last_error.restype = ctypes.c_char_p
     L.kmd_version.argtypes = []
-    for f in ("kmd_decode_filter_fuse", "kmd_decode_filter", "kmd_fuse",
+    for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
+              "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
               "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -119,9 +124,12 @@ def _stream(t: torch.Tensor, stream) -> int:
 def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
                        blend: Optional[torch.Tensor], sizes: Sequence[int],
                        out: Optional[torch.Tensor] = None, blend_is_logits: bool = True,
-                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+                       stream: Optional[torch.cuda.Stream] = None,
+                       albedo: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Fused Eq. 3 -> 4 -> 5: radiance [N,3,H,W], importance [N,M,H,W],
-    blend [N,M,H,W] (None iff M==1) -> out [N,3,H,W] (fp32, CUDA)."""
+    blend [N,M,H,W] (None iff M==1) -> out [N,3,H,W] (fp32, CUDA).  With
+    ``albedo`` [N,3,H,W] the result is remodulated in the same pass
+    (out = Rhat * albedo, PAPER.md:181, 258)."""
     N, C, H, W = radiance.shape
     M = len(sizes)
     rp = _dev_f32("radiance", radiance, (N, 3, H, W))
@@ -131,8 +139,40 @@ def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
         out = torch.empty((N, 3, H, W), device=radiance.device, dtype=torch.float32)
     op = _dev_f32("out", out, (N, 3, H, W))
     cfg = make_config(sizes, blend_is_logits)
-    _check(lib().kmd_decode_filter_fuse(rp, ip, bp, op, N, H, W, ctypes.byref(cfg),
-                                        _stream(radiance, stream)))
+    if albedo is None:
+        _check(lib().kmd_decode_filter_fuse(rp, ip, bp, op, N, H, W, ctypes.byref(cfg),
+                                            _stream(radiance, stream)))
+    else:
+        ap = _dev_f32("albedo", albedo, (N, 3, H, W))
+        _check(lib().kmd_decode_filter_fuse_remod(rp, ip, bp, ap, op, N, H, W, ctypes.byref(cfg),
+                                                  _stream(radiance, stream)))
+    return out
+
+
+def demodulate(radiance: torch.Tensor, albedo: torch.Tensor, eps: float = 1e-3,
+               out: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """irradiance = radiance / max(albedo, eps) (SPEC.md:127-136), [N,3,H,W] CUDA."""
+    N, _, H, W = radiance.shape
+    rp = _dev_f32("radiance", radiance, (N, 3, H, W))
+    ap = _dev_f32("albedo", albedo, (N, 3, H, W))
+    if out is None:
+        out = torch.empty_like(radiance)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    _check(lib().kmd_demodulate(rp, ap, float(eps), op, N, H, W, _stream(radiance, stream)))
+    return out
+
+
+def remodulate(irradiance: torch.Tensor, albedo: torch.Tensor, out: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """out = irradiance * albedo (SPEC.md:138-145), [N,3,H,W] CUDA."""
+    N, _, H, W = irradiance.shape
+    xp = _dev_f32("irradiance", irradiance, (N, 3, H, W))
+    ap = _dev_f32("albedo", albedo, (N, 3, H, W))
+    if out is None:
+        out = torch.empty_like(irradiance)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    _check(lib().kmd_remodulate(xp, ap, op, N, H, W, _stream(irradiance, stream)))
     return out
 
 

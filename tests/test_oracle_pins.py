@@ -326,3 +326,25 @@ def test_softmax_stays_finite_for_huge_importance(oracle_mod):
     assert np.all(np.isfinite(km))
     np.testing.assert_allclose(km.sum(-1), 1.0, rtol=0, atol=1e-15)
     assert km[3, 3, 8] == 1.0 and km[0, 0, 0] == pytest.approx(1 / 9, rel=1e-15)
+
+
+# ------------------------------------------- albedo demod/remod (NEXT row 1)
+def test_demodulate_remodulate_spec_examples(oracle_mod):
+    # SPEC.md:132-135 and 141-144 examples
+    r = np.array([0.6, 0.001, 2.0], np.float32)
+    a = np.array([0.3, 0.0, 1.0], np.float32)
+    d = oracle_mod.demodulate(r, a, eps=1e-3)
+    assert d[0] == pytest.approx(2.0, rel=1e-7)      # 0.6 / 0.3 (fp32 inputs)
+    assert d[1] == pytest.approx(1.0, rel=1e-7)      # eps floor: 0.001 / 1e-3
+    assert d[2] == 2.0                               # albedo 1 -> identity
+    m = oracle_mod.remodulate(np.array([2.0, 5.0]), np.array([0.3, 1.0], np.float32))
+    assert m[0] == pytest.approx(0.6, rel=1e-7) and m[1] == 5.0
+
+
+def test_demod_remod_round_trip(oracle_mod):
+    # remodulate(demodulate(r)) = r wherever albedo >= eps
+    rng = np.random.default_rng(3)
+    r = rng.exponential(1.0, 1000).astype(np.float32)
+    a = rng.uniform(0.01, 1.0, 1000).astype(np.float32)
+    back = oracle_mod.remodulate(oracle_mod.demodulate(r, a, 1e-3), a)
+    np.testing.assert_allclose(back, r.astype(np.float64), rtol=1e-15)
