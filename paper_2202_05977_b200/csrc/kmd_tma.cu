@@ -453,8 +453,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     IWAIT(5, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
                     if (c >= RMAX && c < RMAX + TW) {
                         float* bcol = &sm.bl[sb].B[0][c - RMAX + XOFF];
-#pragma unroll 4
-                        for (int r = 0; r < TH; ++r) bcol[r * BW] = exp_acc(bcol[r * BW]);
+                        float bv[TH];
+#pragma unroll
+                        for (int r = 0; r < TH; ++r) bv[r] = bcol[r * BW];  // all loads first (ILP)
+#pragma unroll
+                        for (int r = 0; r < TH; ++r) bcol[r * BW] = exp_acc(bv[r]);
                     }
                 }
                 if (border_rows && !(p.debug & 4)) {
