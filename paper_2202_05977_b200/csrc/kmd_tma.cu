@@ -239,21 +239,21 @@ struct Acc {
 };
 
 // Eq. 5 with alpha = softmax(B), accumulated one size
-// at a time.  The field warps have already replaced the blend logits B_i by
-// a_i = exp(B_i) (unshifted: any shift cancels in the softmax, reading R2),
-// so here  acc += a_i R_i,  S += a_i,  and Rhat = acc / S at the end.  A
+// at a time: a_i = exp(B_i) (unshifted: any shift cancels in the softmax,
+// reading R2), acc += a_i R_i, S += a_i, and Rhat = acc / S at the end.  A
 // logit beyond the fp32 exp range (S = 0 or inf, non-finite acc) or a tiny box
 // denominator sends the pixel to the exact path (reading R13).
 enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2 };
 
 template <int MODE>
-__device__ __forceinline__ void fuse_px(Acc& st, int j, float a, float4 v) {
+__device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alpha */, float4 v) {
     st.dmin[j] = fminf(st.dmin[j], v.x);
     const float rden = rcp_approx(v.x);
     float w;
     if constexpr (MODE == FUSE_ONE) {
         w = rden;
     } else if constexpr (MODE == FUSE_SOFTMAX) {
+        a = exp_acc(a);  // the blend logit -> exp(B_i), unshifted (reading R2)
         st.S[j] += a;
         w = a * rden;
     } else {  // alpha given (blend_is_logits == 0)
@@ -446,20 +446,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 InSlot& in = sm.in[si];
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
                 IWAIT(4, mbar_wait(&sm.in_full[si], (seq / NI) & 1));
-                if (has_blend && p.blend_is_logits && !(p.debug & 64)) {
-                    // a_i = exp(B_i) for the output columns of this lane (reading
-                    // R2: the softmax shift cancels), in place in the blend box
-                    const int sb = seq % NB;
-                    IWAIT(5, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
-                    if (c >= RMAX && c < RMAX + TW) {
-                        float* bcol = &sm.bl[sb].B[0][c - RMAX + XOFF];
-                        float bv[TH];
-#pragma unroll
-                        for (int r = 0; r < TH; ++r) bv[r] = bcol[r * BW];  // all loads first (ILP)
-#pragma unroll
-                        for (int r = 0; r < TH; ++r) bcol[r * BW] = exp_acc(bv[r]);
-                    }
-                }
                 if (border_rows && !(p.debug & 4)) {
                     fix_rows(&in.I[0][cc], FH * BW, 1, top, bot);
                     fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
