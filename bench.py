@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
-    ap.add_argument("--mode", choices=["frame", "band"], default="frame",
+    ap.add_argument("--mode", choices=["frame", "band", "mr"], default="frame",
                     help="frame: one frame per rank per step (weak scaling, default); band: ONE "
                          "frame split into row bands across ranks with an NCCL halo exchange "
                          "every step (strong scaling, BASELINE.json configs[3], default 4K)")
@@ -457,6 +457,67 @@ def run_band(args, rank, world, local):
         flush=True)
 
 
+def run_mr(args, rank, world, local):
+    """NEXT row 2: "Ours MR" (3 levels x sizes {3,5} + Eq. 7) on a 1080p frame
+    per rank per step (weak scaling), CUDA-graph launched like the main mode."""
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    H, W = args.height, args.width
+    sizes = [list(s) for s in gen.MR_SIZES]
+    K, Wm, F = args.steps, args.warmup, 2
+    frames = [gen.make_mr_inputs(1, H, W, seed=gen.BASE_SEED + 11 + 97 * (rank * F + f), device=dev)
+              for f in range(F)]
+    outs = [torch.empty((1, 3, H, W), device=dev) for _ in range(F)]
+    ws = torch.empty(kmd.mr_workspace_bytes(1, H, W, sizes), dtype=torch.uint8, device=dev)
+
+    def step(s):
+        mi = frames[s % F]
+        kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, sizes,
+                                  out=outs[s % F], workspace=ws)
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for j in range(2 * F):
+            step(j)
+    reps = max(1, K // (2 * F))
+    g.replay()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    steps = reps * 2 * F
+    el = max_over_ranks(a.elapsed_time(b), world)
+    if rank != 0:
+        return
+    # inputs + output, each read/written once: radiance 12, level-l maps
+    # (2 importance + 2 logits) 16 / 4^l, alpha 4 / 4^l (l < 2), out 12
+    algo = H * W * (12 + 12 + sum((16 + (4 if l < 2 else 0)) / 4 ** l for l in range(3)))
+    ms = el / steps
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s (Ours MR: 3 levels x sizes {{3,5}} + Eq. 7)", "value": H * W * steps * world / (el / 1e3) / 1e6,
+        "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": Wm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{W}x{H} multi-resolution reconstruction (NEXT row 2)",
+                                        "levels": 3, "sizes": sizes},
+        "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": measured_peak_hbm()[0],
+                     "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / measured_peak_hbm()[0],
+                     "algorithmic_bytes_per_launch": algo,
+                     "note": "7 launches per step (2 downsample, 3 fused, 2 combine); algorithmic = inputs + output once"},
+        "clocks": clk.summary(), "gpu_launches": steps * 7,
+        "paper_context": "Ours MR reconstruction 0.85 ms at 1280x720 on an RTX 2080 Ti (PAPER.md:435)"}),
+        flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup()
@@ -465,6 +526,8 @@ def main():
             run_reference(args, rank, world)
         elif args.mode == "band":
             run_band(args, rank, world, local)
+        elif args.mode == "mr":
+            run_mr(args, rank, world, local)
         else:
             run_kmd(args, rank, world, local)
     finally:

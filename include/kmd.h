@@ -159,6 +159,42 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
                                        void* device_workspace, size_t workspace_bytes,
                                        kmd_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT row 2: the multi-resolution "Ours MR" reconstruction (PAPER.md:313-318
+ * §5.2, Eq. 7; 324 "two filtering kernels with sizes 3 and 5 for each
+ * resolution"; Table 3).  Level 0 is the input resolution; level
+ * l filters r_l = D^l(r_0) (D = 2x2 mean) with its own
+ * importance maps and fusion logits (Eq. 3-5), then the levels are combined
+ * from the coarsest:  c_{L-1} = f_{L-1},
+ *   c_l = f_l - alpha_l * U D f_l + alpha_l * U c_{l+1}     (Eq. 7)
+ * with U = nearest upsampling.  H and W must be divisible by
+ * 2^(levels-1) (else KMD_ERR_DIM).
+ *   radiance      [N,3,H,W]                      level-0 irradiance
+ *   importance[l] [N,M_l,H>>l,W>>l]              per level (array of device pointers)
+ *   blend[l]      [N,M_l,H>>l,W>>l] or NULL iff M_l == 1
+ *   alpha[l]      [N,1,H>>l,W>>l], l < levels-1  Eq. 7 blending weight in [0,1]
+ *   out           [N,3,H,W]
+ *   workspace     device scratch of kmd_mr_workspace_bytes(...) bytes        */
+#define KMD_MR_MAX_LEVELS 4
+typedef struct {
+    int32_t levels;                          /* 1..KMD_MR_MAX_LEVELS (paper: 3) */
+    kmd_config level[KMD_MR_MAX_LEVELS];     /* sizes per level (paper: {3,5})  */
+} kmd_mr_config;
+size_t kmd_mr_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_mr_config* cfg);
+kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* importance,
+                                     const float* const* blend, const float* const* alpha,
+                                     float* out, int32_t N, int32_t H, int32_t W,
+                                     const kmd_mr_config* cfg, void* workspace,
+                                     size_t workspace_bytes, kmd_stream_t stream);
+/* The two MR building blocks on their own: D on [N,C,H,W] ->
+ * [N,C,H/2,W/2] (H, W even), and Eq. 7 for one pair of levels:
+ * fine [N,3,H,W], coarse [N,3,H/2,W/2], alpha [N,1,H,W] -> out [N,3,H,W].   */
+kmd_status kmd_downsample2x2(const float* in, float* out, int32_t N, int32_t C, int32_t H,
+                             int32_t W, kmd_stream_t stream);
+kmd_status kmd_combine_resolutions(const float* fine, const float* coarse, const float* alpha,
+                                   float* out, int32_t N, int32_t H, int32_t W,
+                                   kmd_stream_t stream);
+
 /* Algorithmic HBM bytes of one kmd_decode_filter_fuse call:
  * N*H*W*4*(3 + M + (blend? M : 0) + 3)  (inputs read once, output written once). */
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,

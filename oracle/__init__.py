@@ -65,9 +65,13 @@ def _load():
         lib.kmdo_max_threads.argtypes = []
         lib.kmdo_demodulate.argtypes = [P, P, ctypes.c_double, ctypes.c_int64, P]
         lib.kmdo_remodulate.argtypes = [P, P, ctypes.c_int64, P]
+        lib.kmdo_downsample_2x2.argtypes = [P, ctypes.c_int64, i32, i32, P]
+        lib.kmdo_upsample_nearest.argtypes = [P, ctypes.c_int64, i32, i32, P]
+        lib.kmdo_combine_resolutions.argtypes = [P, P, P, i32, i32, i32, P]
         for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
                   "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
-                  "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate"):
+                  "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate", "kmdo_downsample_2x2",
+                  "kmdo_upsample_nearest", "kmdo_combine_resolutions"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -205,3 +209,50 @@ def remodulate(irradiance, albedo) -> np.ndarray:
     out = np.empty(x.shape, dtype=np.float64)
     _check(_load().kmdo_remodulate(_ptr(x), _ptr(a), x.size, _ptr(out)))
     return out
+
+
+# ---------------------------------- multi-resolution "Ours MR" (NEXT row 2)
+def downsample_2x2(img) -> np.ndarray:
+    """D of Eq. 7: [..., H, W] fp32 -> [..., H/2, W/2] fp64 block means."""
+    a = _f32(img)
+    H, W = a.shape[-2:]
+    out = np.empty(a.shape[:-2] + (H // 2, W // 2), dtype=np.float64)
+    _check(_load().kmdo_downsample_2x2(_ptr(a), a.size // (H * W), H, W, _ptr(out)))
+    return out
+
+
+def upsample_nearest(img) -> np.ndarray:
+    """U of Eq. 7: [..., h, w] -> [..., 2h, 2w] (fp64)."""
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = a.shape[-2:]
+    out = np.empty(a.shape[:-2] + (2 * h, 2 * w), dtype=np.float64)
+    _check(_load().kmdo_upsample_nearest(_ptr(a), a.size // (h * w), h, w, _ptr(out)))
+    return out
+
+
+def combine_resolutions(fine, coarse, alpha) -> np.ndarray:
+    """Eq. 7 (PAPER.md:316-318): fine [N,3,H,W], coarse [N,3,H/2,W/2], alpha [N,1,H,W]."""
+    f = np.ascontiguousarray(fine, dtype=np.float64)
+    c = np.ascontiguousarray(coarse, dtype=np.float64)
+    a = _f32(alpha)
+    N, _, H, W = f.shape
+    out = np.empty_like(f)
+    _check(_load().kmdo_combine_resolutions(_ptr(f), _ptr(c), _ptr(a), N, H, W, _ptr(out)))
+    return out
+
+
+def mr_decode_filter_fuse(radiance, importance, blend, alpha, sizes, threads: int = 0) -> np.ndarray:
+    """"Ours MR": level l filters D^l(radiance) with importance[l], blend[l]
+    (Eq. 3-5), then Eq. 7 combines from the coarsest level.  The downsampled
+    radiance is rounded to fp32 between levels (the GPU path stores it in fp32,
+    so both sides filter the same level inputs)."""
+    L = len(importance)
+    rad = [_f32(radiance)]
+    for _ in range(1, L):
+        rad.append(downsample_2x2(rad[-1]).astype(np.float32))
+    f = [decode_filter_fuse(rad[l], importance[l], None if blend is None else blend[l], sizes[l],
+                            threads=threads) for l in range(L)]
+    c = f[L - 1]
+    for l in range(L - 2, -1, -1):
+        c = combine_resolutions(f[l], c, alpha[l])
+    return c

@@ -332,6 +332,62 @@ int kmdo_remodulate(const double* irradiance, const float* albedo, int64_t count
     return KMDO_OK;
 }
 
+/* ---- multi-resolution (Eq. 7) -- */
+int kmdo_downsample_2x2(const float* in, int64_t planes, int32_t H, int32_t W, double* out) {
+    if (!in || !out) return KMDO_ERR_NULL;
+    if (H < 2 || W < 2 || (H % 2) || (W % 2)) return KMDO_ERR_DIM;
+    const int h = H / 2, w = W / 2;
+    for (int64_t p = 0; p < planes; ++p)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                const float* s = in + ((size_t)p * H + 2 * y) * W + 2 * x;
+                /* arithmetic mean of the 2x2 source block */
+                out[((size_t)p * h + y) * w + x] =
+                    ((double)s[0] + (double)s[1] + (double)s[W] + (double)s[W + 1]) / 4.0;
+            }
+    return KMDO_OK;
+}
+
+int kmdo_upsample_nearest(const double* in, int64_t planes, int32_t h, int32_t w, double* out) {
+    if (!in || !out) return KMDO_ERR_NULL;
+    if (h < 1 || w < 1) return KMDO_ERR_DIM;
+    const int H = 2 * h, W = 2 * w;
+    for (int64_t p = 0; p < planes; ++p)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x)
+                out[((size_t)p * H + y) * W + x] = in[((size_t)p * h + y / 2) * w + x / 2];
+    return KMDO_OK;
+}
+
+int kmdo_combine_resolutions(const double* fine, const double* coarse, const float* alpha, int32_t N,
+                             int32_t H, int32_t W, double* out) {
+    if (!fine || !coarse || !alpha || !out) return KMDO_ERR_NULL;
+    if (N < 1 || H < 2 || W < 2 || (H % 2) || (W % 2)) return KMDO_ERR_DIM;
+    const size_t plane = (size_t)H * W, cplane = plane / 4;
+    const int h = H / 2, w = W / 2;
+    double* dfine = (double*)malloc(sizeof(double) * cplane);
+    double* udf = (double*)malloc(sizeof(double) * plane);
+    double* uc = (double*)malloc(sizeof(double) * plane);
+    if (!dfine || !udf || !uc) { free(dfine); free(udf); free(uc); return KMDO_ERR_NOMEM; }
+    for (int n = 0; n < N; ++n)
+        for (int c = 0; c < 3; ++c) {
+            const double* f = fine + ((size_t)n * 3 + c) * plane;
+            /* D(fine): the 2x2 mean, in fp64 */
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x)
+                    dfine[(size_t)y * w + x] = (f[(size_t)2 * y * W + 2 * x] + f[(size_t)2 * y * W + 2 * x + 1] +
+                                                f[(size_t)(2 * y + 1) * W + 2 * x] +
+                                                f[(size_t)(2 * y + 1) * W + 2 * x + 1]) / 4.0;
+            kmdo_upsample_nearest(dfine, 1, h, w, udf);
+            kmdo_upsample_nearest(coarse + ((size_t)n * 3 + c) * cplane, 1, h, w, uc);
+            const float* a = alpha + (size_t)n * plane;
+            double* o = out + ((size_t)n * 3 + c) * plane;
+            for (size_t q = 0; q < plane; ++q) o[q] = f[q] - (double)a[q] * udf[q] + (double)a[q] * uc[q];
+        }
+    free(dfine); free(udf); free(uc);
+    return KMDO_OK;
+}
+
 int kmdo_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -91,6 +91,16 @@ int kmdo_demodulate(const float* radiance, const float* albedo, double eps, int6
  * albedo"): out[t] = irradiance[t] * albedo[t]. */
 int kmdo_remodulate(const double* irradiance, const float* albedo, int64_t count, double* out);
 
+/* ---- multi-resolution "Ours MR" (§5.2, Eq. 7) ----------
+ * D: 2x2 mean downsampling: in [P][H][W] -> out [P][H/2][W/2]. */
+int kmdo_downsample_2x2(const float* in, int64_t planes, int32_t H, int32_t W, double* out);
+/* U: nearest upsampling: in [P][h][w] (fp64) -> out [P][2h][2w]. */
+int kmdo_upsample_nearest(const double* in, int64_t planes, int32_t h, int32_t w, double* out);
+/* Eq. 7: out = fine - alpha * U(D(fine)) + alpha * U(coarse),
+ * fine [N][3][H][W] (fp64), coarse [N][3][H/2][W/2] (fp64), alpha [N][H][W]. */
+int kmdo_combine_resolutions(const double* fine, const double* coarse, const float* alpha, int32_t N,
+                             int32_t H, int32_t W, double* out);
+
 /* Threads OpenMP would use for threads <= 0 (reported as cpu_baseline.cores). */
 int kmdo_max_threads(void);
 

@@ -405,6 +405,112 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     return KMD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NEXT row 2: multi-resolution reconstruction (Eq. 7)
+static size_t mr_level_floats(int N, int H, int W, int l) {
+    return (size_t)N * 3 * (size_t)(H >> l) * (size_t)(W >> l);
+}
+
+size_t kmd_mr_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_mr_config* cfg) {
+    if (!cfg || cfg->levels < 1 || cfg->levels > KMD_MR_MAX_LEVELS || N < 1 || H < 1 || W < 1) return 0;
+    // r_l (l >= 1), f_l (all l), c_l (1 <= l < levels-1), each rounded to 32 floats
+    size_t f = 0;
+    for (int l = 0; l < cfg->levels; ++l) {
+        const size_t n = (mr_level_floats(N, H, W, l) + 31) & ~(size_t)31;
+        f += n;                                    // f_l
+        if (l >= 1) f += n;                        // r_l
+        if (l >= 1 && l < cfg->levels - 1) f += n; // c_l
+    }
+    return f * sizeof(float);
+}
+
+kmd_status kmd_downsample2x2(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t W,
+                             kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0 || C < 0) return fail(KMD_ERR_DIM, "N=%d, C=%d must be >= 0", N, C);
+    if (N == 0 || C == 0) return KMD_OK;
+    if (H < 2 || W < 2 || (H & 1) || (W & 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be even and >= 2", H, W);
+    if (!in || !out) return fail(KMD_ERR_NULL, "NULL buffer");
+    const size_t ib = (size_t)N * C * H * W * sizeof(float);
+    if (overlaps(out, ib / 4, in, ib)) return fail(KMD_ERR_ALIAS, "out overlaps in");
+    cudaError_t e = kmd::launch_down2(in, out, (long long)N * C, H / 2, W / 2, (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "downsample launch");
+}
+
+kmd_status kmd_combine_resolutions(const float* fine, const float* coarse, const float* alpha, float* out,
+                                   int32_t N, int32_t H, int32_t W, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N == 0) return KMD_OK;
+    if (H < 2 || W < 2 || (H & 1) || (W & 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be even and >= 2", H, W);
+    if (!fine || !coarse || !alpha || !out) return fail(KMD_ERR_NULL, "NULL buffer");
+    const size_t fb = (size_t)N * 3 * H * W * sizeof(float);
+    if (overlaps(out, fb, fine, fb) || overlaps(out, fb, coarse, fb / 4) || overlaps(out, fb, alpha, fb / 3))
+        return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    cudaError_t e = kmd::launch_combine(fine, coarse, alpha, out, N, H, W, (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "combine launch");
+}
+
+kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* importance,
+                                     const float* const* blend, const float* const* alpha, float* out,
+                                     int32_t N, int32_t H, int32_t W, const kmd_mr_config* cfg,
+                                     void* workspace, size_t workspace_bytes, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    const int L = cfg->levels;
+    if (L < 1 || L > KMD_MR_MAX_LEVELS) return fail(KMD_ERR_CONFIG, "levels=%d not in [1,%d]", L, KMD_MR_MAX_LEVELS);
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N == 0) return KMD_OK;
+    const int mask = (1 << (L - 1)) - 1;
+    if (H < 1 || W < 1 || (H & mask) || (W & mask))
+        return fail(KMD_ERR_DIM, "H=%d, W=%d must be divisible by 2^(levels-1)=%d", H, W, mask + 1);
+    for (int l = 0; l < L; ++l) {
+        kmd_status s = check_cfg(&cfg->level[l], H >> l, W >> l);
+        if (s) return s;
+    }
+    if (!radiance || !importance || !out || !workspace || (L > 1 && !alpha))
+        return fail(KMD_ERR_NULL, "NULL argument");
+    for (int l = 0; l < L; ++l) {
+        if (!importance[l]) return fail(KMD_ERR_NULL, "importance[%d] is NULL", l);
+        if (cfg->level[l].num_sizes > 1 && (!blend || !blend[l])) return fail(KMD_ERR_NULL, "blend[%d] is NULL", l);
+        if (l < L - 1 && !alpha[l]) return fail(KMD_ERR_NULL, "alpha[%d] is NULL", l);
+    }
+    if (workspace_bytes < kmd_mr_workspace_bytes(N, H, W, cfg))
+        return fail(KMD_ERR_DIM, "workspace %zu bytes < required %zu", workspace_bytes,
+                    kmd_mr_workspace_bytes(N, H, W, cfg));
+    cudaStream_t st = (cudaStream_t)stream;
+    // carve the workspace: for each level l: f_l, r_l (l>=1), c_l (1<=l<L-1)
+    float* ws = (float*)workspace;
+    float *r[KMD_MR_MAX_LEVELS] = {}, *f[KMD_MR_MAX_LEVELS] = {}, *c[KMD_MR_MAX_LEVELS] = {};
+    for (int l = 0; l < L; ++l) {
+        const size_t n = (mr_level_floats(N, H, W, l) + 31) & ~(size_t)31;
+        f[l] = ws; ws += n;
+        if (l >= 1) { r[l] = ws; ws += n; }
+        if (l >= 1 && l < L - 1) { c[l] = ws; ws += n; }
+    }
+    r[0] = const_cast<float*>(radiance);
+    cudaError_t e;
+    for (int l = 1; l < L; ++l)
+        if ((e = kmd::launch_down2(r[l - 1], r[l], (long long)N * 3, H >> l, W >> l, st)) != cudaSuccess)
+            return cuda_fail(e, "downsample launch");
+    for (int l = 0; l < L; ++l) {
+        float* dst = (L == 1) ? out : f[l];
+        kmd_status s = kmd_decode_filter_fuse(r[l], importance[l], blend ? blend[l] : nullptr, dst, N, H >> l,
+                                              W >> l, &cfg->level[l], stream);
+        if (s) return s;
+    }
+    if (L == 1) return KMD_OK;
+    // Eq. 7 from the coarsest level: c_{L-1} = f_{L-1}; c_l = combine(f_l, c_{l+1}, alpha_l)
+    const float* coarse = f[L - 1];
+    for (int l = L - 2; l >= 0; --l) {
+        float* dst = (l == 0) ? out : c[l];
+        if ((e = kmd::launch_combine(f[l], coarse, alpha[l], dst, N, H >> l, W >> l, st)) != cudaSuccess)
+            return cuda_fail(e, "combine launch");
+        coarse = dst;
+    }
+    return KMD_OK;
+}
+
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
                               int32_t has_blend) {
     if (!cfg || N < 0 || H < 0 || W < 0) return -1;

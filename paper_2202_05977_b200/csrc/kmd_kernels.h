@@ -23,4 +23,9 @@ cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* o
 cudaError_t launch_albedo_op(const float* x, const float* albedo, float eps, float* out, long long n, int op,
                              cudaStream_t stream);
 
+// multi-resolution ("Ours MR", NEXT row 2; kmd_mr.cu)
+cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, int Wo, cudaStream_t st);
+cudaError_t launch_combine(const float* fine, const float* coarse, const float* alpha, float* out, int N, int H,
+                           int W, cudaStream_t st);
+
 }  // namespace kmd

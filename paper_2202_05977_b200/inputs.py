@@ -120,3 +120,39 @@ def make_albedo(N: int, H: int, W: int, seed: int = BASE_SEED + 7, frame_offset:
         zero = torch.rand((1, H, W), generator=g, device=device) < 0.01
         out.append(torch.where(zero, torch.zeros_like(a), a))
     return torch.stack(out).contiguous()
+
+
+MR_SIZES = ((3, 5), (3, 5), (3, 5))  # "two filtering kernels with sizes 3 and 5 for each resolution"
+
+
+@dataclass
+class MRInputs:
+    radiance: torch.Tensor   # [N,3,H,W]
+    importance: list         # per level [N,2,H>>l,W>>l]
+    blend: list              # per level [N,2,H>>l,W>>l]
+    alpha: list              # per level l < L-1: [N,1,H>>l,W>>l] in [0,1]
+
+
+def make_mr_inputs(N: int, H: int, W: int, sizes_per_level=MR_SIZES, seed: int = BASE_SEED + 11,
+                   device="cpu") -> MRInputs:
+    """Inputs of the multi-resolution variant (NEXT row 2): per level the same
+    importance / logit recipe as make_inputs, and Eq. 7 blend weights
+    alpha = sigmoid(1.5 * smooth + N(0, 0.5^2)) in [0, 1]."""
+    L = len(sizes_per_level)
+    base = make_inputs(N, H, W, len(sizes_per_level[0]), seed=seed, device=device)
+    imps, blends, alphas = [base.importance], [base.blend], []
+    for l in range(1, L):
+        lv = make_inputs(N, H >> l, W >> l, len(sizes_per_level[l]), seed=seed + 1000 * l,
+                         device=device)
+        imps.append(lv.importance)
+        blends.append(lv.blend)
+    device = torch.device(device)
+    for l in range(L - 1):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed + 5000 + l)
+        h, w = H >> l, W >> l
+        a = torch.stack([torch.sigmoid(1.5 * _smooth(g, 1, h, w, device) +
+                                       0.5 * torch.randn((1, h, w), generator=g, device=device))
+                         for _ in range(N)])
+        alphas.append(a.contiguous())
+    return MRInputs(base.radiance, imps, blends, alphas)

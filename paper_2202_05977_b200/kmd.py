@@ -49,9 +49,26 @@ def make_config(sizes: Sequence[int], blend_is_logits: bool = True) -> kmd_confi
     return cfg
 
 
+KMD_MR_MAX_LEVELS = 4
+
+
+class kmd_mr_config(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("level", kmd_config * KMD_MR_MAX_LEVELS)]
+
+
+def make_mr_config(sizes_per_level: Sequence[Sequence[int]]) -> kmd_mr_config:
+    cfg = kmd_mr_config()
+    cfg.levels = len(sizes_per_level)
+    for l, sz in enumerate(list(sizes_per_level)[:KMD_MR_MAX_LEVELS]):
+        cfg.level[l] = make_config(sz)
+    return cfg
+
+
 _lib = None
 
 EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
+           "kmd_mr_workspace_bytes", "kmd_mr_decode_filter_fuse", "kmd_downsample2x2",
+           "kmd_combine_resolutions",
            "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
            "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
@@ -75,6 +92,13 @@ def lib(build_if_missing: bool = True):
     L.kmd_demodulate.argtypes = [P, P, ctypes.c_float, P, i32, i32, i32, P]
     L.kmd_remodulate.argtypes = [P, P, P, i32, i32, i32, P]
     L.kmd_decode_filter.argtypes = [P, P, P, i32, i32, i32, i32, P]
+    MC = ctypes.POINTER(kmd_mr_config)
+    L.kmd_mr_workspace_bytes.argtypes = [i32, i32, i32, MC]
+    L.kmd_mr_workspace_bytes.restype = ctypes.c_size_t
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    L.kmd_mr_decode_filter_fuse.argtypes = [P, PP, PP, PP, P, i32, i32, i32, MC, P, ctypes.c_size_t, P]
+    L.kmd_downsample2x2.argtypes = [P, P, i32, i32, i32, i32, P]
+    L.kmd_combine_resolutions.argtypes = [P, P, P, P, i32, i32, i32, P]
     L.kmd_fuse.argtypes = [P, P, P, i32, i32, i32, i32, i32, P]
     L.kmd_decode_filter_fuse_band.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, P]
     L.kmd_host_workspace_bytes.argtypes = [i32, i32, i32, C]
@@ -89,7 +113,8 @@ def lib(build_if_missing: bool = True):
     L.kmd_last_error.restype = ctypes.c_char_p
     L.kmd_version.argtypes = []
     for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
-              "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
+              "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
+              "kmd_downsample2x2", "kmd_combine_resolutions",
               "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -278,3 +303,69 @@ def launches_per_call() -> int:
 
 def version() -> int:
     return int(lib().kmd_version())
+
+
+# --------------------------------------------- multi-resolution (NEXT row 2)
+def mr_workspace_bytes(N: int, H: int, W: int, sizes_per_level) -> int:
+    cfg = make_mr_config(sizes_per_level)
+    return int(lib().kmd_mr_workspace_bytes(N, H, W, ctypes.byref(cfg)))
+
+
+def mr_decode_filter_fuse(radiance: torch.Tensor, importance, blend, alpha, sizes_per_level,
+                          out: Optional[torch.Tensor] = None,
+                          workspace: Optional[torch.Tensor] = None,
+                          stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """"Ours MR" (PAPER.md:313-318, Eq. 7): radiance [N,3,H,W]; importance[l],
+    blend[l] [N,M_l,H>>l,W>>l]; alpha[l] [N,1,H>>l,W>>l] for l < levels-1."""
+    N, _, H, W = radiance.shape
+    L = len(sizes_per_level)
+    rp = _dev_f32("radiance", radiance, (N, 3, H, W))
+    ip = (ctypes.c_void_p * L)(*[_dev_f32(f"importance[{l}]", importance[l],
+                                         (N, len(sizes_per_level[l]), H >> l, W >> l))
+                                 for l in range(L)])
+    bp = None
+    if blend is not None:
+        bp = (ctypes.c_void_p * L)(*[None if blend[l] is None else
+                                     _dev_f32(f"blend[{l}]", blend[l],
+                                              (N, len(sizes_per_level[l]), H >> l, W >> l))
+                                     for l in range(L)])
+    ap = (ctypes.c_void_p * max(1, L - 1))(*[_dev_f32(f"alpha[{l}]", alpha[l], (N, 1, H >> l, W >> l))
+                                             for l in range(L - 1)])
+    if out is None:
+        out = torch.empty((N, 3, H, W), device=radiance.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    cfg = make_mr_config(sizes_per_level)
+    need = int(lib().kmd_mr_workspace_bytes(N, H, W, ctypes.byref(cfg)))
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=radiance.device)
+    _check(lib().kmd_mr_decode_filter_fuse(
+        rp, ctypes.cast(ip, ctypes.POINTER(ctypes.c_void_p)),
+        None if bp is None else ctypes.cast(bp, ctypes.POINTER(ctypes.c_void_p)),
+        ctypes.cast(ap, ctypes.POINTER(ctypes.c_void_p)), op, N, H, W, ctypes.byref(cfg),
+        workspace.data_ptr(), workspace.numel(), _stream(radiance, stream)))
+    return out
+
+
+def downsample2x2(x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    N, C, H, W = x.shape
+    xp = _dev_f32("in", x)
+    if out is None:
+        out = torch.empty((N, C, H // 2, W // 2), device=x.device, dtype=torch.float32)
+    op = _dev_f32("out", out, (N, C, H // 2, W // 2))
+    _check(lib().kmd_downsample2x2(xp, op, N, C, H, W, _stream(x, stream)))
+    return out
+
+
+def combine_resolutions(fine: torch.Tensor, coarse: torch.Tensor, alpha: torch.Tensor,
+                        out: Optional[torch.Tensor] = None,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    N, _, H, W = fine.shape
+    fp = _dev_f32("fine", fine, (N, 3, H, W))
+    cp = _dev_f32("coarse", coarse, (N, 3, H // 2, W // 2))
+    ap = _dev_f32("alpha", alpha, (N, 1, H, W))
+    if out is None:
+        out = torch.empty_like(fine)
+    op = _dev_f32("out", out, (N, 3, H, W))
+    _check(lib().kmd_combine_resolutions(fp, cp, ap, op, N, H, W, _stream(fine, stream)))
+    return out

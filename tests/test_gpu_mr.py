@@ -1,0 +1,51 @@
+"""NEXT row 2: the multi-resolution "Ours MR" reconstruction
+(Eq. 7; 3 levels x sizes {3,5}) vs the fp64
+oracle.  Eq. 7 subtracts (f - alpha U D f), so the bound is relative to the
+magnitude of the terms: |gpu - ref| <= 1e-5 * (|f| + alpha |U D f| + alpha |U c|)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2202_05977_b200 import inputs as gen
+from paper_2202_05977_b200 import kmd
+from parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(t, d):
+    return None if t is None else t.to(d)
+
+
+@pytest.mark.parametrize("N,H,W", [(1, 96, 160), (2, 72, 104), (1, 36, 44)])
+def test_mr_matches_oracle(oracle_mod, cuda_device, N, H, W):
+    sizes = [list(s) for s in gen.MR_SIZES]
+    mi = gen.make_mr_inputs(N, H, W)
+    out = kmd.mr_decode_filter_fuse(mi.radiance.to(cuda_device),
+                                    [_dev(t, cuda_device) for t in mi.importance],
+                                    [_dev(t, cuda_device) for t in mi.blend],
+                                    [_dev(t, cuda_device) for t in mi.alpha], sizes)
+    torch.cuda.synchronize()
+    ref = oracle_mod.mr_decode_filter_fuse(mi.radiance.numpy(), [t.numpy() for t in mi.importance],
+                                           [t.numpy() for t in mi.blend], [t.numpy() for t in mi.alpha],
+                                           sizes)
+    # scale of the Eq. 7 terms at level 0: the level-0 filtered image bounds them
+    f0 = oracle_mod.decode_filter_fuse(mi.radiance.numpy(), mi.importance[0].numpy(),
+                                       mi.blend[0].numpy(), sizes[0])
+    scale = np.abs(ref) + 2 * np.abs(f0) + 1e-30
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref) / scale
+    assert np.all(np.isfinite(out.cpu().numpy()))
+    assert err.max() <= 1e-5, err.max()
+
+
+def test_downsample_and_combine_entry_points(oracle_mod, cuda_device):
+    x = gen.make_inputs(2, 40, 52, 1).radiance
+    d = kmd.downsample2x2(x.to(cuda_device))
+    torch.cuda.synchronize()
+    assert_parity(d.cpu().numpy(), oracle_mod.downsample_2x2(x.numpy()), tol=3e-7, what="D")
+    fine = gen.make_inputs(1, 40, 52, 1, seed=5).radiance
+    coarse = gen.make_inputs(1, 20, 26, 1, seed=6).radiance
+    alpha = torch.zeros((1, 1, 40, 52))
+    o = kmd.combine_resolutions(fine.to(cuda_device), coarse.to(cuda_device), alpha.to(cuda_device))
+    torch.cuda.synchronize()
+    assert torch.equal(o.cpu(), fine)       # alpha = 0 -> fine, exactly

@@ -348,3 +348,43 @@ def test_demod_remod_round_trip(oracle_mod):
     a = rng.uniform(0.01, 1.0, 1000).astype(np.float32)
     back = oracle_mod.remodulate(oracle_mod.demodulate(r, a, 1e-3), a)
     np.testing.assert_allclose(back, r.astype(np.float64), rtol=1e-15)
+
+
+# ---------------------------------------- multi-resolution "Ours MR" (NEXT row 2)
+def test_downsample_upsample_spec_examples(oracle_mod):
+    # [1,2,3,4] -> 2.5; constant -> constant; block mean brute force
+    assert oracle_mod.downsample_2x2(np.array([[1, 2], [3, 4]], np.float32))[0, 0] == 2.5
+    c = np.full((6, 8), 0.75, np.float32)
+    assert np.all(oracle_mod.downsample_2x2(c) == 0.75)
+    x = RNG.standard_normal((2, 8, 10)).astype(np.float32)
+    ref = x.astype(np.float64).reshape(2, 4, 2, 5, 2).mean(axis=(2, 4))
+    np.testing.assert_allclose(oracle_mod.downsample_2x2(x), ref, rtol=1e-15, atol=1e-15)
+    # U replicates; U(D(constant)) = identity; min/max preserved
+    u = oracle_mod.upsample_nearest(np.array([[7.0]]))
+    assert u.shape == (2, 2) and np.all(u == 7.0)
+    y = RNG.standard_normal((3, 4, 5))
+    uy = oracle_mod.upsample_nearest(y)
+    assert np.array_equal(uy[:, ::2, ::2], y) and np.array_equal(uy[:, 1::2, 1::2], y)
+
+
+def test_combine_resolutions_spec_examples(oracle_mod):
+    # SPEC.md:303-306 / Eq. 7
+    N, H, W = 1, 8, 6
+    fine = RNG.exponential(1.0, (N, 3, H, W))
+    coarse = RNG.exponential(1.0, (N, 3, H // 2, W // 2))
+    zero = np.zeros((N, 1, H, W), np.float32)
+    assert np.array_equal(oracle_mod.combine_resolutions(fine, coarse, zero), fine)   # alpha = 0
+    a = RNG.uniform(0, 1, (N, 1, H, W)).astype(np.float32)
+    dfine = oracle_mod.downsample_2x2(fine.astype(np.float32)).astype(np.float64)
+    f32 = fine.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(oracle_mod.combine_resolutions(f32, dfine, a), f32, rtol=1e-15)  # coarse = D(fine)
+    one = np.ones((N, 1, H, W), np.float32)
+    out = oracle_mod.combine_resolutions(np.full((N, 3, H, W), 2.0), np.full((N, 3, H // 2, W // 2), 5.0), one)
+    assert np.all(out == 5.0)                                                           # alpha = 1, constants
+
+
+def test_mr_single_level_is_plain_decoder(oracle_mod):
+    rad, imp, blend = _rand_inputs(8, 12, 2, RNG)
+    a = oracle_mod.mr_decode_filter_fuse(rad, [imp], [blend], [], [[3, 5]])
+    b = oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 5])
+    assert np.array_equal(a, b)
