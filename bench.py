@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
-    ap.add_argument("--mode", choices=["frame", "band", "mr"], default="frame",
+    ap.add_argument("--mode", choices=["frame", "band", "mr", "bwd"], default="frame",
                     help="frame: one frame per rank per step (weak scaling, default); band: ONE "
                          "frame split into row bands across ranks with an NCCL halo exchange "
                          "every step (strong scaling, BASELINE.json configs[3], default 4K)")
@@ -518,6 +518,68 @@ def run_mr(args, rank, world, local):
         flush=True)
 
 
+def run_bwd(args, rank, world, local):
+    """NEXT row 3: backward (dL/dI, dL/dB given dL/dRhat) on a 1080p frame per
+    rank per step (weak scaling), CUDA-graph launched like the main mode."""
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    H, W = args.height, args.width
+    sizes = [int(x) for x in args.sizes.split(",")]
+    M = len(sizes)
+    K, Wm, F = args.steps, args.warmup, 2
+    frames = [gen.make_inputs(1, H, W, M, frame_offset=rank * F + f, device=dev) for f in range(F)]
+    grads = [torch.randn((1, 3, H, W), device=dev) for _ in range(F)]
+    gI = [torch.empty((1, M, H, W), device=dev) for _ in range(F)]
+    gB = [torch.empty((1, M, H, W), device=dev) for _ in range(F)]
+    ws = torch.empty(kmd.backward_workspace_bytes(1, H, W, sizes), dtype=torch.uint8, device=dev)
+
+    def step(s):
+        fi = frames[s % F]
+        kmd.decode_filter_fuse_backward(fi.radiance, fi.importance, fi.blend, grads[s % F], sizes,
+                                        grad_importance=gI[s % F], grad_blend=gB[s % F], workspace=ws)
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for j in range(2 * F):
+            step(j)
+    reps = max(1, K // (2 * F))
+    g.replay()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    steps = reps * 2 * F
+    el = max_over_ranks(a.elapsed_time(b), world)
+    if rank != 0:
+        return
+    # read radiance 12, importance 4M, logits 4M, grad_out 12; write dL/dI 4M, dL/dB 4M
+    algo = H * W * (24 + 16 * M)
+    ms = el / steps
+    peak = measured_peak_hbm()[0]
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s (backward: dL/dI, dL/dB)", "value": H * W * steps * world / (el / 1e3) / 1e6,
+        "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": Wm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{W}x{H} backward of the fused decoder (NEXT row 3)",
+                                        "sizes": sizes},
+        "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / peak,
+                     "algorithmic_bytes_per_launch": algo,
+                     "note": f"{kmd.backward_launches_per_call(M)} launches per step; algorithmic = inputs + outputs once"},
+        "clocks": clk.summary(), "gpu_launches": steps * kmd.backward_launches_per_call(M)}),
+        flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup()
@@ -528,6 +590,8 @@ def main():
             run_band(args, rank, world, local)
         elif args.mode == "mr":
             run_mr(args, rank, world, local)
+        elif args.mode == "bwd":
+            run_bwd(args, rank, world, local)
         else:
             run_kmd(args, rank, world, local)
     finally:

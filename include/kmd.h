@@ -195,6 +195,23 @@ kmd_status kmd_combine_resolutions(const float* fine, const float* coarse, const
                                    float* out, int32_t N, int32_t H, int32_t W,
                                    kmd_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT row 3: backward of kmd_decode_filter_fuse w.r.t. the importance maps
+ * and the fusion logits (end-to-end training, Eq. 1;
+ * SPEC.md:289-297).  Given grad_out = dL/dRhat [N,3,H,W] (device):
+ *   grad_importance [N,M,H,W] = dL/dI_i,  grad_blend [N,M,H,W] = dL/dB_i
+ *   (dL/dalpha_i when blend_is_logits == 0; may be NULL; zeros when M == 1).
+ * The radiance gradient is not computed (rendered data).  The
+ * forward box sums are recomputed; importance must lie in (-80, 80).  Needs a
+ * device workspace of kmd_backward_workspace_bytes(...) bytes.              */
+size_t kmd_backward_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg);
+kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* importance,
+                                           const float* blend, const float* grad_out,
+                                           float* grad_importance, float* grad_blend, int32_t N,
+                                           int32_t H, int32_t W, const kmd_config* cfg,
+                                           void* workspace, size_t workspace_bytes,
+                                           kmd_stream_t stream);
+
 /* Algorithmic HBM bytes of one kmd_decode_filter_fuse call:
  * N*H*W*4*(3 + M + (blend? M : 0) + 3)  (inputs read once, output written once). */
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,

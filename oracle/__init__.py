@@ -68,10 +68,11 @@ def _load():
         lib.kmdo_downsample_2x2.argtypes = [P, ctypes.c_int64, i32, i32, P]
         lib.kmdo_upsample_nearest.argtypes = [P, ctypes.c_int64, i32, i32, P]
         lib.kmdo_combine_resolutions.argtypes = [P, P, P, i32, i32, i32, P]
+        lib.kmdo_backward.argtypes = [P, P, P, P, i32, i32, i32, i32, P, i32, P, P]
         for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
                   "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
                   "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate", "kmdo_downsample_2x2",
-                  "kmdo_upsample_nearest", "kmdo_combine_resolutions"):
+                  "kmdo_upsample_nearest", "kmdo_combine_resolutions", "kmdo_backward"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -256,3 +257,20 @@ def mr_decode_filter_fuse(radiance, importance, blend, alpha, sizes, threads: in
     for l in range(L - 2, -1, -1):
         c = combine_resolutions(f[l], c, alpha[l])
     return c
+
+
+# ------------------------------------------------------- backward (NEXT row 3)
+def backward(radiance, importance, blend, grad_out, sizes, blend_is_logits: bool = True):
+    """dL/dI [N,M,H,W] and dL/dB [N,M,H,W] (fp64) for L with dL/dRhat = grad_out."""
+    radiance = _f32(radiance)
+    importance = _f32(importance)
+    b = None if blend is None else _f32(blend)
+    G = np.ascontiguousarray(grad_out, dtype=np.float64)
+    N, _, H, W = radiance.shape
+    M = importance.shape[1]
+    sz = np.ascontiguousarray(sizes, dtype=np.int32)
+    gI = np.empty((N, M, H, W), dtype=np.float64)
+    gB = np.empty((N, M, H, W), dtype=np.float64)
+    _check(_load().kmdo_backward(_ptr(radiance), _ptr(importance), _ptr(b), _ptr(G), N, H, W, M,
+                                 _ptr(sz), int(bool(blend_is_logits)), _ptr(gI), _ptr(gB)))
+    return gI, gB

@@ -388,6 +388,82 @@ int kmdo_combine_resolutions(const double* fine, const double* coarse, const flo
     return KMDO_OK;
 }
 
+/* ---- backward (NEXT row 3) ---------------------------------------------- */
+int kmdo_backward(const float* radiance, const float* importance, const float* blend,
+                  const double* grad_out, int32_t N, int32_t H, int32_t W, int32_t M,
+                  const int32_t* sizes, int32_t blend_is_logits, double* grad_imp,
+                  double* grad_blend) {
+    if (!grad_out || !grad_imp) return KMDO_ERR_NULL;
+    int st = check_all(radiance, importance, blend, N, H, W, M, sizes);
+    if (st) return st;
+    const size_t plane = (size_t)H * W;
+    memset(grad_imp, 0, sizeof(double) * (size_t)N * M * plane);
+    if (grad_blend) memset(grad_blend, 0, sizeof(double) * (size_t)N * M * plane);
+    scratch_t s;
+    st = scratch_alloc(&s, M, sizes);
+    if (st) { scratch_free(&s); return st; }
+    int kkmax = 1;
+    for (int i = 0; i < M; ++i)
+        if (sizes[i] * sizes[i] > kkmax) kkmax = sizes[i] * sizes[i];
+    double* wall = (double*)malloc(sizeof(double) * (size_t)M * kkmax);  /* w of every size */
+    int* qyall = (int*)malloc(sizeof(int) * (size_t)M * kkmax);
+    int* qxall = (int*)malloc(sizeof(int) * (size_t)M * kkmax);
+    if (!wall || !qyall || !qxall) { free(wall); free(qyall); free(qxall); scratch_free(&s); return KMDO_ERR_NOMEM; }
+    for (int n = 0; n < N; ++n)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                const float* rad = radiance + (size_t)n * 3 * plane;
+                /* forward, Steps 1-3 per size (as pixel()) keeping the weights */
+                for (int i = 0; i < M; ++i) {
+                    const int k = sizes[i], kk = k * k;
+                    const float* Ii = importance + ((size_t)n * M + i) * plane;
+                    unfold_pixel(Ii, H, W, k, y, x, s.u, qyall + i * kkmax, qxall + i * kkmax);
+                    softmax_window(s.u, kk, wall + i * kkmax);
+                    apply_window(wall + i * kkmax, qyall + i * kkmax, qxall + i * kkmax, kk, rad, H, W,
+                                 s.Ri + 3 * i);
+                }
+                /* Step 4 weights */
+                double alpha[64], b[64];
+                for (int i = 0; i < M; ++i)
+                    b[i] = blend ? (double)blend[((size_t)n * M + i) * plane + (size_t)y * W + x] : 0.0;
+                if (M == 1) {
+                    alpha[0] = 1.0;
+                } else if (blend_is_logits) {
+                    double beta = b[0], sum = 0.0;
+                    for (int i = 1; i < M; ++i) if (b[i] > beta) beta = b[i];
+                    for (int i = 0; i < M; ++i) { alpha[i] = exp(b[i] - beta); sum += alpha[i]; }
+                    for (int i = 0; i < M; ++i) alpha[i] /= sum;
+                } else {
+                    for (int i = 0; i < M; ++i) alpha[i] = b[i];
+                }
+                double Rh[3] = {0, 0, 0};
+                for (int i = 0; i < M; ++i)
+                    for (int c = 0; c < 3; ++c) Rh[c] += alpha[i] * s.Ri[3 * i + c];
+                double G[3];
+                for (int c = 0; c < 3; ++c) G[c] = grad_out[((size_t)n * 3 + c) * plane + (size_t)y * W + x];
+                for (int i = 0; i < M; ++i) {
+                    const int kk = sizes[i] * sizes[i];
+                    if (grad_blend && M > 1) {
+                        double v = 0.0;
+                        for (int c = 0; c < 3; ++c)
+                            v += blend_is_logits ? alpha[i] * G[c] * (s.Ri[3 * i + c] - Rh[c]) : G[c] * s.Ri[3 * i + c];
+                        grad_blend[((size_t)n * M + i) * plane + (size_t)y * W + x] = v;
+                    }
+                    double* gI = grad_imp + ((size_t)n * M + i) * plane;
+                    for (int j = 0; j < kk; ++j) {
+                        const int qy = qyall[i * kkmax + j], qx = qxall[i * kkmax + j];
+                        double acc = 0.0;
+                        for (int c = 0; c < 3; ++c)
+                            acc += alpha[i] * G[c] * ((double)rad[c * plane + (size_t)qy * W + qx] - s.Ri[3 * i + c]);
+                        gI[(size_t)qy * W + qx] += wall[i * kkmax + j] * acc;
+                    }
+                }
+            }
+    free(wall); free(qyall); free(qxall);
+    scratch_free(&s);
+    return KMDO_OK;
+}
+
 int kmdo_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

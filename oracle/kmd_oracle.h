@@ -101,6 +101,19 @@ int kmdo_upsample_nearest(const double* in, int64_t planes, int32_t h, int32_t w
 int kmdo_combine_resolutions(const double* fine, const double* coarse, const float* alpha, int32_t N,
                              int32_t H, int32_t W, double* out);
 
+/* ---- backward (NEXT row 3; Eq. 1) ----
+ * Chain rule of Eq. 3 -> 4 -> 5 in the explicit-kernel form, one output pixel
+ * at a time (serial):  with G = grad_out(p), alpha = softmax(B(p)),
+ *   grad_blend_i(p)   = alpha_i sum_c G_c (R_i,c - Rhat_c)   (logits)
+ *                     = sum_c G_c R_i,c                      (alpha given; 0 when M == 1)
+ *   grad_imp_i(q_j)  += w_j sum_c alpha_i G_c (r_c(q_j) - R_i,c)   for every tap j of p's window
+ * (dR/du_j of a softmax-weighted mean is w_j (r(q_j) - R); u_j = I_i(q_j)).
+ * grad_out [N,3,H,W] fp64; grad_imp [N,M,H,W]; grad_blend [N,M,H,W] or NULL. */
+int kmdo_backward(const float* radiance, const float* importance, const float* blend,
+                  const double* grad_out, int32_t N, int32_t H, int32_t W, int32_t M,
+                  const int32_t* sizes, int32_t blend_is_logits, double* grad_imp,
+                  double* grad_blend);
+
 /* Threads OpenMP would use for threads <= 0 (reported as cpu_baseline.cores). */
 int kmdo_max_threads(void);
 

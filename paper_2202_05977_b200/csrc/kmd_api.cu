@@ -511,6 +511,37 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
     return KMD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// NEXT row 3: backward
+size_t kmd_backward_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg) {
+    if (!cfg || N < 1 || H < 1 || W < 1 || cfg->num_sizes < 1 || cfg->num_sizes > KMD_MAX_SIZES) return 0;
+    return kmd::bwd_workspace_floats(H, W, cfg->num_sizes) * sizeof(float);
+}
+
+kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* importance, const float* blend,
+                                           const float* grad_out, float* grad_importance, float* grad_blend,
+                                           int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                                           void* workspace, size_t workspace_bytes, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (N > 0) {
+        kmd_status s = check_cfg(cfg, H, W);
+        if (s) return s;
+    }
+    if (N == 0) return KMD_OK;
+    if (!radiance || !importance || !grad_out || !grad_importance || !workspace)
+        return fail(KMD_ERR_NULL, "NULL argument");
+    if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (workspace_bytes < kmd_backward_workspace_bytes(N, H, W, cfg))
+        return fail(KMD_ERR_DIM, "workspace too small");
+    cudaError_t e = kmd::launch_backward(radiance, importance, cfg->num_sizes > 1 ? blend : nullptr, grad_out,
+                                         grad_importance, grad_blend, N, H, W, cfg->num_sizes, cfg->sizes,
+                                         cfg->blend_is_logits, (float*)workspace, (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "backward launch");
+}
+
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
                               int32_t has_blend) {
     if (!cfg || N < 0 || H < 0 || W < 0) return -1;

@@ -28,4 +28,10 @@ cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, 
 cudaError_t launch_combine(const float* fine, const float* coarse, const float* alpha, float* out, int N, int H,
                            int W, cudaStream_t st);
 
+// backward (NEXT row 3; kmd_bwd.cu)
+size_t bwd_workspace_floats(int H, int W, int M);
+cudaError_t launch_backward(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
+                            float* gB, int N, int H, int W, int M, const int* sizes, int logits, float* ws,
+                            cudaStream_t st);
+
 }  // namespace kmd

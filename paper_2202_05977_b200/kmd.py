@@ -68,7 +68,8 @@ _lib = None
 
 EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
            "kmd_mr_workspace_bytes", "kmd_mr_decode_filter_fuse", "kmd_downsample2x2",
-           "kmd_combine_resolutions",
+           "kmd_combine_resolutions", "kmd_backward_workspace_bytes",
+           "kmd_decode_filter_fuse_backward",
            "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
            "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
@@ -100,6 +101,9 @@ def lib(build_if_missing: bool = True):
     L.kmd_downsample2x2.argtypes = [P, P, i32, i32, i32, i32, P]
     L.kmd_combine_resolutions.argtypes = [P, P, P, P, i32, i32, i32, P]
     L.kmd_fuse.argtypes = [P, P, P, i32, i32, i32, i32, i32, P]
+    L.kmd_backward_workspace_bytes.argtypes = [i32, i32, i32, C]
+    L.kmd_backward_workspace_bytes.restype = ctypes.c_size_t
+    L.kmd_decode_filter_fuse_backward.argtypes = [P, P, P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
     L.kmd_decode_filter_fuse_band.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, P]
     L.kmd_host_workspace_bytes.argtypes = [i32, i32, i32, C]
     L.kmd_host_workspace_bytes.restype = ctypes.c_size_t
@@ -114,7 +118,7 @@ def lib(build_if_missing: bool = True):
     L.kmd_version.argtypes = []
     for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
               "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
-              "kmd_downsample2x2", "kmd_combine_resolutions",
+              "kmd_downsample2x2", "kmd_combine_resolutions", "kmd_decode_filter_fuse_backward",
               "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -369,3 +373,67 @@ def combine_resolutions(fine: torch.Tensor, coarse: torch.Tensor, alpha: torch.T
     op = _dev_f32("out", out, (N, 3, H, W))
     _check(lib().kmd_combine_resolutions(fp, cp, ap, op, N, H, W, _stream(fine, stream)))
     return out
+
+
+# ------------------------------------------------------- backward (NEXT row 3)
+def backward_workspace_bytes(N: int, H: int, W: int, sizes: Sequence[int]) -> int:
+    cfg = make_config(sizes)
+    return int(lib().kmd_backward_workspace_bytes(N, H, W, ctypes.byref(cfg)))
+
+
+def decode_filter_fuse_backward(radiance: torch.Tensor, importance: torch.Tensor,
+                                blend: Optional[torch.Tensor], grad_out: torch.Tensor,
+                                sizes: Sequence[int], blend_is_logits: bool = True,
+                                grad_importance: Optional[torch.Tensor] = None,
+                                grad_blend: Optional[torch.Tensor] = None,
+                                workspace: Optional[torch.Tensor] = None,
+                                stream: Optional[torch.cuda.Stream] = None):
+    """dL/dI [N,M,H,W] and dL/dB [N,M,H,W] (None when blend is None) given
+    grad_out = dL/dRhat [N,3,H,W] (Eq. 1: the decoder is
+    trained end to end through Eq. 3-5)."""
+    N, _, H, W = radiance.shape
+    M = len(sizes)
+    rp = _dev_f32("radiance", radiance, (N, 3, H, W))
+    ip = _dev_f32("importance", importance, (N, M, H, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, H, W))
+    gp = _dev_f32("grad_out", grad_out, (N, 3, H, W))
+    if grad_importance is None:
+        grad_importance = torch.empty((N, M, H, W), device=radiance.device, dtype=torch.float32)
+    gip = _dev_f32("grad_importance", grad_importance, (N, M, H, W))
+    gbp = None
+    if blend is not None:
+        if grad_blend is None:
+            grad_blend = torch.empty((N, M, H, W), device=radiance.device, dtype=torch.float32)
+        gbp = _dev_f32("grad_blend", grad_blend, (N, M, H, W))
+    cfg = make_config(sizes, blend_is_logits)
+    need = int(lib().kmd_backward_workspace_bytes(N, H, W, ctypes.byref(cfg)))
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=radiance.device)
+    _check(lib().kmd_decode_filter_fuse_backward(rp, ip, bp, gp, gip, gbp, N, H, W, ctypes.byref(cfg),
+                                                 workspace.data_ptr(), workspace.numel(),
+                                                 _stream(radiance, stream)))
+    return grad_importance, grad_blend
+
+
+def backward_launches_per_call(M: int) -> int:
+    """Kernel launches of one single-frame decode_filter_fuse_backward call."""
+    return 5 * M + 1
+
+
+class DecodeFilterFuse(torch.autograd.Function):
+    """Differentiable kmd_decode_filter_fuse (w.r.t. importance and blend):
+    forward and backward both run in libkmd."""
+
+    @staticmethod
+    def forward(ctx, radiance, importance, blend, sizes, blend_is_logits=True):
+        ctx.sizes = tuple(sizes)
+        ctx.logits = blend_is_logits
+        ctx.save_for_backward(radiance, importance, blend)
+        return decode_filter_fuse(radiance, importance, blend, sizes, blend_is_logits=blend_is_logits)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        radiance, importance, blend = ctx.saved_tensors
+        gI, gB = decode_filter_fuse_backward(radiance, importance, blend, grad_out.contiguous(),
+                                             ctx.sizes, ctx.logits)
+        return None, gI, gB, None, None

@@ -1,0 +1,112 @@
+"""NEXT row 3: gradients of the fused decoder w.r.t. the
+importance maps and the fusion logits (Eq. 1 — the kernel
+maps are trained end to end through Eq. 3-5), GPU vs the fp64 oracle
+(oracle.backward, pinned to torch autograd and central differences in
+test_oracle_pins.py).
+
+Tolerance (backward): dL/dI_i(q) = e(q)[sum_c r_c T_c - T_R]
+is a difference of two fp32 box-transposed sums of similar size, so its
+error is relative to the map's scale, not to each element: we require
+|gpu - ref| <= BWD_TOL * max|ref| over each (frame, size) map, BWD_TOL = 1e-4
+(~1000 ulp: two k-tap fp32 sums per axis, a division and the cancellation).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2202_05977_b200 import inputs as gen
+from paper_2202_05977_b200 import kmd
+
+pytestmark = pytest.mark.gpu
+PAPER = list(gen.PAPER_SIZES)
+BWD_TOL = 1e-4
+
+
+def _normwise(gpu, ref, what):
+    gpu = np.asarray(gpu, np.float64)
+    assert np.all(np.isfinite(gpu)), f"{what}: non-finite"
+    worst = 0.0
+    for n in range(ref.shape[0]):
+        for i in range(ref.shape[1]):
+            s = np.abs(ref[n, i]).max()
+            d = np.abs(gpu[n, i] - ref[n, i]).max()
+            e = d / s if s > 0 else d
+            worst = max(worst, e)
+            assert e <= BWD_TOL, f"{what}[{n},{i}]: normwise err {e:.3e} > {BWD_TOL}"
+    return worst
+
+
+@pytest.mark.parametrize("N,H,W,sizes,logits", [
+    (1, 96, 160, PAPER, True),
+    (2, 37, 53, [3, 5, 7], True),
+    (1, 40, 44, [3, 9], False),
+    (1, 33, 70, [5], True),
+    (1, 3, 17, [3], True),
+    (1, 5, 3, [3, 3], True),   # smallest legal frames: k <= min(H, W) (DESIGN.md R-readings)
+])
+def test_backward_matches_oracle(oracle_mod, cuda_device, N, H, W, sizes, logits):
+    M = len(sizes)
+    inp = gen.make_inputs(N, H, W, M, seed=21, with_blend=M > 1)
+    blend = inp.blend
+    if blend is not None and not logits:
+        blend = torch.softmax(blend, dim=1).contiguous()
+    G = torch.randn((N, 3, H, W), generator=torch.Generator().manual_seed(5), dtype=torch.float32)
+    dev = cuda_device
+    gI, gB = kmd.decode_filter_fuse_backward(inp.radiance.to(dev), inp.importance.to(dev),
+                                             None if blend is None else blend.to(dev), G.to(dev),
+                                             sizes, blend_is_logits=logits)
+    torch.cuda.synchronize()
+    rI, rB = oracle_mod.backward(inp.radiance.numpy(), inp.importance.numpy(),
+                                 None if blend is None else blend.numpy(), G.numpy().astype(np.float64),
+                                 sizes, blend_is_logits=logits)
+    e = _normwise(gI.cpu().numpy(), rI, "grad_importance")
+    print(f"grad_importance normwise err {e:.3e}")
+    if M > 1:
+        e = _normwise(gB.cpu().numpy(), rB, "grad_blend")
+        print(f"grad_blend normwise err {e:.3e}")
+    else:
+        assert gB is None
+
+
+def test_backward_1080p_invariants(cuda_device):
+    # full paper size: shift invariance of Eq. 3 / Eq. 5 (sums of gradients ~ 0)
+    # and finiteness.  Per pixel, sum_i dL/dB_i = sum_i alpha_i G.(R_i - Rhat) = 0
+    # and its fp32 terms are bounded by sum_i alpha_i |G|.(R_i + Rhat) = 2 |G|.Rhat
+    # (radiance >= 0), so that is the scale of the rounding.
+    inp = gen.make_inputs(1, 1080, 1920, 6, seed=22, device=cuda_device)
+    G = torch.randn((1, 3, 1080, 1920), device=cuda_device)
+    gI, gB = kmd.decode_filter_fuse_backward(inp.radiance, inp.importance, inp.blend, G, PAPER)
+    torch.cuda.synchronize()
+    assert torch.isfinite(gI).all() and torch.isfinite(gB).all()
+    gI64, gB64 = gI.double(), gB.double()
+    rel_I = (gI64.sum(dim=(2, 3)).abs() / gI64.abs().sum(dim=(2, 3))).max().item()
+    Rhat = kmd.decode_filter_fuse(inp.radiance, inp.importance, inp.blend, PAPER).double()
+    scale_B = 2 * (G.double().abs() * Rhat).sum(dim=1)
+    rel_B = (gB64.sum(dim=1).abs() / scale_B.clamp_min(1e-30)).max().item()
+    assert rel_I < 1e-4, rel_I
+    assert rel_B < 1e-5, rel_B
+
+
+def test_autograd_function(oracle_mod, cuda_device):
+    sizes = [3, 5, 7]
+    inp = gen.make_inputs(1, 48, 64, 3, seed=23)
+    I = inp.importance.to(cuda_device).requires_grad_(True)
+    B = inp.blend.to(cuda_device).requires_grad_(True)
+    out = kmd.DecodeFilterFuse.apply(inp.radiance.to(cuda_device), I, B, sizes)
+    G = torch.randn_like(out)
+    (out * G).sum().backward()
+    rI, rB = oracle_mod.backward(inp.radiance.numpy(), inp.importance.numpy(), inp.blend.numpy(),
+                                 G.cpu().numpy().astype(np.float64), sizes)
+    _normwise(I.grad.cpu().numpy(), rI, "autograd grad_importance")
+    _normwise(B.grad.cpu().numpy(), rB, "autograd grad_blend")
+
+
+def test_backward_empty_and_errors(cuda_device):
+    z = torch.empty((0, 3, 8, 8), device=cuda_device)
+    zi = torch.empty((0, 2, 8, 8), device=cuda_device)
+    gI, gB = kmd.decode_filter_fuse_backward(z, zi, zi.clone(), z.clone(), [3, 5])
+    assert gI.shape == (0, 2, 8, 8)
+    inp = gen.make_inputs(1, 8, 8, 2, seed=1, device=cuda_device)
+    with pytest.raises(RuntimeError):
+        kmd.decode_filter_fuse_backward(inp.radiance, inp.importance, inp.blend,
+                                        torch.zeros_like(inp.radiance), [3, 4])

@@ -388,3 +388,98 @@ def test_mr_single_level_is_plain_decoder(oracle_mod):
     a = oracle_mod.mr_decode_filter_fuse(rad, [imp], [blend], [], [[3, 5]])
     b = oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 5])
     assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------ backward (NEXT row 3)
+def _torch_forward_fp64(rad, imp, blend, sizes, logits=True):
+    """Eq. 3-5 written with torch library steps (replicate pad + F.unfold,
+    softmax), independent of the C oracle's loops; autograd differentiates it."""
+    import torch
+    import torch.nn.functional as F
+    N, _, H, W = rad.shape
+    out = 0.0
+    Rs = []
+    for i, k in enumerate(sizes):
+        r = (k - 1) // 2
+        Ii = F.pad(imp[:, i:i + 1], (r, r, r, r), mode="replicate")
+        rp = F.pad(rad, (r, r, r, r), mode="replicate")
+        u = F.unfold(Ii, k).view(N, 1, k * k, H, W)
+        w = torch.softmax(u, dim=2)
+        v = F.unfold(rp, k).view(N, 3, k * k, H, W)
+        Rs.append((w * v).sum(dim=2))
+    if len(sizes) == 1:
+        return Rs[0]
+    a = torch.softmax(blend, dim=1) if logits else blend
+    for i, R in enumerate(Rs):
+        out = out + a[:, i:i + 1] * R
+    return out
+
+
+@pytest.mark.parametrize("sizes,logits", [((3, 5), True), ((5,), True), ((3, 5, 7), False)])
+def test_backward_matches_autograd_of_library_forward(oracle_mod, sizes, logits):
+    # pin: torch autograd of an unfold/softmax forward in fp64 (PAPER.md:128-130 Eq. 1:
+    # the decoder is trained end to end, so its gradients are those of Eq. 3-5).
+    import torch
+    rng = np.random.default_rng(31)
+    M = len(sizes)
+    rad, imp, blend = _rand_inputs(9, 11, M, rng)
+    if not logits:
+        blend = rng.uniform(0, 1, size=blend.shape).astype(np.float32)
+    G = rng.standard_normal((1, 3, 9, 11))
+    gI, gB = oracle_mod.backward(rad, imp, blend, G, sizes, blend_is_logits=logits)
+    ti = torch.tensor(imp, dtype=torch.float64, requires_grad=True)
+    tb = torch.tensor(blend, dtype=torch.float64, requires_grad=True)
+    out = _torch_forward_fp64(torch.tensor(rad, dtype=torch.float64), ti, tb, sizes, logits)
+    (out * torch.tensor(G)).sum().backward()
+    np.testing.assert_allclose(gI, ti.grad.numpy(), rtol=1e-10, atol=1e-12)
+    if M > 1:
+        np.testing.assert_allclose(gB, tb.grad.numpy(), rtol=1e-10, atol=1e-12)
+    else:
+        assert np.all(gB == 0)
+
+
+def test_backward_central_differences(oracle_mod):
+    # pin: central differences of the (pinned) fp64 forward with exactly
+    # representable perturbations (inputs on a 2^-12 grid, h = 2^-10).
+    rng = np.random.default_rng(32)
+    sizes = (3, 5)
+    rad, imp, blend = _rand_inputs(6, 7, 2, rng)
+    imp = (np.round(imp * 4096) / 4096).astype(np.float32)
+    blend = (np.round(blend * 4096) / 4096).astype(np.float32)
+    G = rng.standard_normal((1, 3, 6, 7))
+    gI, gB = oracle_mod.backward(rad, imp, blend, G, sizes)
+    h = 2.0 ** -10
+
+    def L(im, bl):
+        return float((oracle_mod.decode_filter_fuse(rad, im, bl, sizes) * G).sum())
+
+    for arr, grad, which in ((imp, gI, 0), (blend, gB, 1)):
+        fd = np.zeros_like(grad)
+        for idx in np.ndindex(arr.shape):
+            p, m = arr.copy(), arr.copy()
+            p[idx] += np.float32(h)
+            m[idx] -= np.float32(h)
+            lp = L(p, blend) if which == 0 else L(imp, p)
+            lm = L(m, blend) if which == 0 else L(imp, m)
+            fd[idx] = (lp - lm) / (2 * h)
+        np.testing.assert_allclose(grad, fd, rtol=0, atol=2e-5 * np.abs(fd).max())
+
+
+def test_backward_invariants(oracle_mod):
+    # shift invariance of Eq. 3 in I_i and of Eq. 5 in B: gradients sum to 0;
+    # constant radiance makes every R_i the same constant -> dL/dI = 0 and dL/dB = 0
+    # (SPEC.md:296); grad_out = 0 -> all zero.
+    rng = np.random.default_rng(33)
+    sizes = (3, 5, 7)
+    rad, imp, blend = _rand_inputs(10, 12, 3, rng)
+    G = rng.standard_normal((1, 3, 10, 12))
+    gI, gB = oracle_mod.backward(rad, imp, blend, G, sizes)
+    scale = np.abs(gI).max()
+    assert scale > 0
+    assert np.abs(gI.sum(axis=(2, 3))).max() < 1e-12 * scale * gI[0, 0].size
+    assert np.abs(gB.sum(axis=1)).max() < 1e-14 * max(1.0, np.abs(gB).max()) * 10
+    crad = np.full_like(rad, 0.625)
+    gI0, gB0 = oracle_mod.backward(crad, imp, blend, G, sizes)
+    assert np.abs(gI0).max() < 1e-14 and np.abs(gB0).max() < 1e-14
+    gI1, gB1 = oracle_mod.backward(rad, imp, blend, np.zeros_like(G), sizes)
+    assert np.all(gI1 == 0) and np.all(gB1 == 0)
