@@ -390,18 +390,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
             constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BW * 4;
-            // In-order, blocking issue (deadlock-free: every wait is on a step
-            // whose inputs were issued earlier).  The blend ring is primed here
-            // and refilled by the fusion warps as they release slots.
-            const int total_seq = my_tiles * M;
-            if (has_blend)
-                for (int q = 0; q < NB && q < total_seq; ++q) {
-                    const int tl = q / M, i = q - tl * M;
-                    const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
-                    mbar_arrive_expect_tx(&sm.b_full[q], B_BYTES);
-                    tma_load_3d(&sm.bl[q].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
-                                &sm.b_full[q]);
-                }
+            // In-order, blocking issue of every (tile, size) step: radiance
+            // (per tile), importance and blend logits.  Deadlock-free: each wait
+            // is on a slot released by a step whose inputs were issued earlier
+            // (the field warps run at most NV steps ahead of the fusion warps,
+            // and the rings are NI, NB >= NV + 1 deep).
             for (int tl = 0; tl < my_tiles; ++tl) {
                 const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
                 const int rb = tl & 1;
@@ -422,6 +415,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES);
                         tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
                                     tc.n * M + i, &sm.in_full[s]);
+                    }
+                    if (has_blend) {
+                        const int sb = seq % NB;
+                        IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
+                        mbar_arrive_expect_tx(&sm.b_full[sb], B_BYTES);
+                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
+                                    &sm.b_full[sb]);
                     }
                 }
             }
@@ -474,11 +474,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
         // ----------------------------------------------------------- fusion
         const int c = threadIdx.x - (1 + NFIELD) * 32;
-        // thread = (row, segment); segments start at 0,7,13,20,26,33,39,46 and
-        // alternate 7/6 pixels; every thread computes 7 (the 7th of a 6-pixel
-        // segment is recomputed by its neighbour and not stored)
+        // thread = (row, segment); segments start at 0,6,12,19,26,33,39,45
+        // (lengths 6,6,7,7,7,6,6,7): the starts are distinct mod 8, so the 8
+        // lanes of a row hit 8 different 16-byte bank groups with every
+        // LDS.128 of V.  Every thread computes 7 pixels (the 7th of a 6-pixel
+        // segment is recomputed by its neighbour and not stored).
         const int ty = c / NSEG, sub = c % NSEG;
-        const int xs = (sub * 13 + 1) >> 1, len = (sub & 1) ? SEG - 1 : SEG;
+        const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
+        const int len = (0x76677766u >> (4 * sub)) & 0xf;
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             // albedo of this thread's pixels, loaded now so the latency hides
@@ -511,20 +514,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (!(p.debug & 64)) fuse_job(p, sl, sm.bl[sb], st, ty, xs, (p.sizes[i] - 1) / 2, i);
                 __syncwarp();
                 if ((c & 31) == 0) mbar_arrive(&sm.v_empty[s]);
-                if (has_blend) {
-                    if ((c & 31) == 0) mbar_arrive(&sm.b_empty[sb]);
-                    // refill this blend slot with step seq + NB once every fusion
-                    // thread has released it
-                    const int nq = seq + NB;
-                    if (c == 0 && nq < my_tiles * M) {
-                        IWAIT(8, mbar_wait(&sm.b_empty[sb], (seq / NB) & 1));
-                        const int ntl = nq / M, ni = nq - ntl * M;
-                        const Tile nt = tile_of(p, blockIdx.x + ntl * gridDim.x, tiles_x, tiles_y);
-                        mbar_arrive_expect_tx(&sm.b_full[sb], TH * BW * 4);
-                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, nt.x0 - XOFF, nt.y0 - p.out_y0, nt.n * M + ni,
-                                    &sm.b_full[sb]);
-                    }
-                }
+                if (has_blend && (c & 31) == 0) mbar_arrive(&sm.b_empty[sb]);
             }
             if (p.debug & 1024) continue;
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
