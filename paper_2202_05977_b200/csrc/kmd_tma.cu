@@ -73,8 +73,12 @@ struct InSlot {
 struct Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
 };
+// blend box: the 52 output columns plus 4 of padding, starting at x0 (no
+// halo); the 56-float row stride puts the 4 rows x 8 segment starts a fusion
+// warp reads at 32 distinct banks
+constexpr int BBW = 56;
 struct BSlot {
-    alignas(128) float B[TH][BW];      // blend logits of map i, rows y0 .. y0+23, cols x0-8 .. x0+59
+    alignas(128) float B[TH][BBW];     // blend logits of map i, rows y0 .. y0+23, cols x0 .. x0+55
 };
 struct RadBuf {
     alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
@@ -178,47 +182,50 @@ __device__ __forceinline__ void gw_line(F&& field, E&& emit) {
     gw_block<R, N, 0>(suf, field, emit);
 }
 
-// Same sums, same order, with the full blocks in a rolled loop (the block
-// body exists once in the code instead of N/K times): ~35% less field code
-// for the paper's radii, which keeps the hot loop closer to the I-cache.
-template <int R, int N, class F, class E>
-__device__ __forceinline__ void gw_line_rolled(F&& field, E&& emit) {
+template <int CNT, class F1>
+__device__ __forceinline__ void fill_field(float4* dst, int base, F1& f1) {
+#pragma unroll
+    for (int t = 0; t < CNT; ++t) dst[t] = f1(base + t);
+}
+
+// The vertical (field-warp) Gil-Werman line: same sums in the same order as
+// gw_line, with the block body in a rolled loop (it exists once in the code
+// instead of N/K times; ~35% less field code for the paper's radii, which
+// keeps the hot loop closer to the I-cache).  (Producing the field values in
+// pairs with packed FP32 exp was measured 2% slower.)
+template <int R, int N, class F1, class E>
+__device__ __forceinline__ void gw_line_field(F1&& f1, E&& emit) {
     constexpr int K = 2 * R + 1;
     constexpr int NBLK = (N + K - 1) / K;
-    if constexpr (NBLK <= 2) {
-        gw_line<R, N>(field, emit);
-    } else {
-        float4 suf[K];
+    float4 suf[K];
+    fill_field<K>(suf, 0, f1);
 #pragma unroll
-        for (int t = 0; t < K; ++t) suf[t] = field(t);
-#pragma unroll
-        for (int t = K - 2; t >= 0; --t) suf[t] = add4(suf[t], suf[t + 1]);
-        // blocks 0 .. NBLK-2: every output and every next-block field index is in range
+    for (int t = K - 2; t >= 0; --t) suf[t] = add4(suf[t], suf[t + 1]);
+    // blocks 0 .. NBLK-2: every output and every next-block field index is in range
 #pragma unroll 1
-        for (int b = 0; b < NBLK - 1; ++b) {
-            const int x0 = b * K;
-            emit(x0, suf[0]);
-            float4 raw[K];
+    for (int b = 0; b < NBLK - 1; ++b) {
+        const int x0 = b * K;
+        emit(x0, suf[0]);
+        float4 raw[K];
+        fill_field<K>(raw, x0 + K, f1);
+        float4 pre = raw[0];
 #pragma unroll
-            for (int t = 0; t < K; ++t) raw[t] = field(x0 + K + t);
-            float4 pre = raw[0];
-#pragma unroll
-            for (int t = 1; t < K; ++t) {
-                if (t > 1) pre = add4(pre, raw[t - 1]);
-                emit(x0 + t, add4(suf[t], pre));
-            }
-#pragma unroll
-            for (int t = K - 2; t >= 0; --t) raw[t] = add4(raw[t], raw[t + 1]);
-#pragma unroll
-            for (int t = 0; t < K; ++t) suf[t] = raw[t];
+        for (int t = 1; t < K; ++t) {
+            if (t > 1) pre = add4(pre, raw[t - 1]);
+            emit(x0 + t, add4(suf[t], pre));
         }
-        // last block: outputs X0 .. N-1
-        constexpr int X0 = (NBLK - 1) * K;
-        constexpr int TMAX = N - 1 - X0;
-        emit(X0, suf[0]);
-        float4 raw[TMAX > 0 ? TMAX : 1];
 #pragma unroll
-        for (int t = 0; t < TMAX; ++t) raw[t] = field(X0 + K + t);
+        for (int t = K - 2; t >= 0; --t) raw[t] = add4(raw[t], raw[t + 1]);
+#pragma unroll
+        for (int t = 0; t < K; ++t) suf[t] = raw[t];
+    }
+    // last block: outputs X0 .. N-1
+    constexpr int X0 = (NBLK - 1) * K;
+    constexpr int TMAX = N - 1 - X0;
+    emit(X0, suf[0]);
+    if constexpr (TMAX > 0) {
+        float4 raw[TMAX];
+        fill_field<TMAX>(raw, X0 + K, f1);
         float4 pre = raw[0];
 #pragma unroll
         for (int t = 1; t <= TMAX; ++t) {
@@ -266,7 +273,7 @@ __device__ __forceinline__ void field_job(Smem& sm, const InSlot& in, Slot& sl, 
     const float* Ib = &in.I[RMAX - R][cc];
     const float* Rb = &sm.rad[rb].v[0][RMAX - R][cc];
     float4* Vc = &sl.V[0][c];
-    gw_line_rolled<R, TH>(
+    gw_line_field<R, TH>(
         [&](int f) {
             const float v = Ib[f * BW];
             const float r = Rb[f * BW], g = Rb[FH * BW + f * BW], b = Rb[2 * FH * BW + f * BW];
@@ -342,7 +349,7 @@ __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, c
         case 5: hbox<5>(sl, ty, xs, o); break;
         default: hbox<6>(sl, ty, xs, o); break;
     }
-    const float* Br = &bs.B[ty][xs + XOFF];
+    const float* Br = &bs.B[ty][xs];
     if constexpr (SMODE >= 0) {
         fuse_seg<SMODE>(st, Br, o);  // mode fixed by the kernel's specialisation
     } else {
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
-            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BW * 4;
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BBW * 4;
             // In-order, blocking issue of every (tile, size) step: radiance
             // (per tile), importance and blend logits.  Deadlock-free: each wait
             // is on a slot released by a step whose inputs were issued earlier
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const int sb = seq % NB;
                         IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
                         mbar_arrive_expect_tx(&sm.b_full[sb], B_BYTES);
-                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0 - XOFF, tc.y0 - p.out_y0, tc.n * M + i,
+                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0, tc.y0 - p.out_y0, tc.n * M + i,
                                     &sm.b_full[sb]);
                     }
                 }
@@ -731,7 +738,7 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
         !make_map(&m_out, p.out, p.W, p.out_rows, 3LL * p.N, TW, TH, 3))
         return cudaErrorInvalidValue;
     if (p.blend) {
-        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BW, TH, 1))
+        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BBW, TH, 1))
             return cudaErrorInvalidValue;
     } else {
         m_blend = m_imp;  // never used
