@@ -284,6 +284,8 @@ __device__ __forceinline__ void field_job(Smem& sm, const InSlot& in, Slot& sl, 
         [&](int oy, float4 v) {
             // two 8-byte stores keep the FADD2 register pairs in place (no MOVs
             // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
+            // (one STS.128 would halve the store wavefronts but costs MOVs to
+            // assemble the quad: measured 7% slower)
             const unsigned a = smem_u32(&Vc[oy * VS]);
             asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
             asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
@@ -437,6 +439,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = SP::M > 0 ? SP::M : p.M;
     const bool has_blend = p.blend != nullptr && !(p.debug & 16);
+    unsigned rpack = 0;  // radius of size i in bits 4i..4i+3
+    for (int i = 0; i < M; ++i) rpack |= (unsigned)((p.sizes[i] - 1) / 2) << (4 * i);
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; ++b) {
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int jl = fw; jl < 2 * M; jl += NFIELD) {
                     const int i = jl >> 1, h = jl & 1;
                     job(i, h, [&](const InSlot& in, Slot& sl, int cc) {
-                        switch ((p.sizes[i] - 1) / 2) {
+                        switch ((rpack >> (4 * i)) & 15) {
                             case 0: field_job<0>(sm, in, sl, rb, h, cc); break;
                             case 1: field_job<1>(sm, in, sl, rb, h, cc); break;
                             case 2: field_job<2>(sm, in, sl, rb, h, cc); break;
@@ -574,6 +578,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int ty = c / NSEG, sub = c % NSEG;
         const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
         const int len = (0x76677766u >> (4 * sub)) & 0xf;
+        int vs = 0, vph = 0, bs = 0, bph = 0;  // V / blend ring slot and phase of the current step
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             // albedo of this thread's pixels, loaded now so the latency hides
@@ -598,18 +603,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 st.a[j][0] = st.a[j][1] = st.a[j][2] = 0.f;
                 st.dmin[j] = INFINITY;
             }
-            {
 #pragma unroll 1
-                for (int i = 0; i < M; ++i) {
-                    const int seq = tl * M + i, s = seq % NV, sb = seq % NB;
-                    IWAIT(6, mbar_wait(&sm.v_full[s], (seq / NV) & 1));
-                    if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
-                    const Slot& sl = sm.slot[s];
-                    if (!(p.debug & 64)) fuse_job<SP::MODE>(p, sl, sm.bl[sb], st, ty, xs, (p.sizes[i] - 1) / 2);
-                    __syncwarp();
-                    if ((c & 31) == 0) mbar_arrive(&sm.v_empty[s]);
-                    if (has_blend && (c & 31) == 0) mbar_arrive(&sm.b_empty[sb]);
+            for (int i = 0; i < M; ++i) {
+                IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
+                if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
+                if (!(p.debug & 64)) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, (rpack >> (4 * i)) & 15);
+                __syncwarp();
+                if ((c & 31) == 0) {
+                    mbar_arrive(&sm.v_empty[vs]);
+                    if (has_blend) mbar_arrive(&sm.b_empty[bs]);
                 }
+                // ring slots and phases of the next (tile, size) step
+                if (++vs == NV) { vs = 0; vph ^= 1; }
+                if (++bs == NB) { bs = 0; bph ^= 1; }
             }
             if (p.debug & 1024) continue;
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
