@@ -531,8 +531,7 @@ kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* i
         if (s) return s;
     }
     if (N == 0) return KMD_OK;
-    if (!radiance || !importance || !grad_out || !grad_importance || !workspace)
-        return fail(KMD_ERR_NULL, "NULL argument");
+    if (!radiance || !importance || !grad_out || !grad_importance) return fail(KMD_ERR_NULL, "NULL argument");
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
     if (workspace_bytes < kmd_backward_workspace_bytes(N, H, W, cfg))
         return fail(KMD_ERR_DIM, "workspace too small");

@@ -416,8 +416,9 @@ def decode_filter_fuse_backward(radiance: torch.Tensor, importance: torch.Tensor
 
 
 def backward_launches_per_call(M: int) -> int:
-    """Kernel launches of one single-frame decode_filter_fuse_backward call."""
-    return 5 * M + 1
+    """Kernel launches of one decode_filter_fuse_backward call (one tiled kernel;
+    plus a memset of grad_blend when M == 1)."""
+    return 1 if M > 1 else 2
 
 
 class DecodeFilterFuse(torch.autograd.Function):

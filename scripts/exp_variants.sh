@@ -8,7 +8,7 @@ run() {
 import sys,json
 l=[x for x in sys.stdin.read().splitlines() if x.startswith('{')]
 d=json.loads(l[-1]) if l else {}
-print(d.get('kernel_ms',{}).get('avg',0)*1000 if d else 'FAIL', 'us', d.get('parity'))"
+print((d.get('kernel_ms',{}).get('avg') or d.get('ms_per_step'))*1000 if d else 'FAIL', 'us', d.get('parity'))"
 }
 echo "base: $(run "$@")"
 for v in scripts/probe/variants/libkmd_*.so; do
