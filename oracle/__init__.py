@@ -42,7 +42,7 @@ def build(force: bool = False) -> str:
     if force or stale:
         tmp = LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
-                               "-Wall", "-Wextra", "-o", tmp, _SRC, "-lm"])
+                               "-ffp-contract=off", "-Wall", "-Wextra", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -69,10 +69,13 @@ def _load():
         lib.kmdo_upsample_nearest.argtypes = [P, ctypes.c_int64, i32, i32, P]
         lib.kmdo_combine_resolutions.argtypes = [P, P, P, i32, i32, i32, P]
         lib.kmdo_backward.argtypes = [P, P, P, P, i32, i32, i32, i32, P, i32, P, P]
+        f32 = ctypes.c_float
+        lib.kmdo_temporal_accumulate.argtypes = [P, P, P, P, P, P, P, P, i32, i32, i32, f32, f32, f32, P, P]
         for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
                   "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
                   "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate", "kmdo_downsample_2x2",
-                  "kmdo_upsample_nearest", "kmdo_combine_resolutions", "kmdo_backward"):
+                  "kmdo_upsample_nearest", "kmdo_combine_resolutions", "kmdo_backward",
+                  "kmdo_temporal_accumulate"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -274,3 +277,20 @@ def backward(radiance, importance, blend, grad_out, sizes, blend_is_logits: bool
     _check(_load().kmdo_backward(_ptr(radiance), _ptr(importance), _ptr(b), _ptr(G), N, H, W, M,
                                  _ptr(sz), int(bool(blend_is_logits)), _ptr(gI), _ptr(gB)))
     return gI, gB
+
+
+# ------------------------------------------------ temporal accumulation (NEXT row 4)
+def temporal_accumulate(cur_rad, prev_rad, prev_pos, prev_nrm, prev_valid, cur_pos, cur_nrm, motion,
+                        pos_tol: float, normal_tol: float = 0.9, alpha: float = 0.2):
+    """reproject + consistency_test + temporal_accumulate (SPEC.md:147-175):
+    returns (accum [N,3,H,W] fp64, mask [N,H,W] uint8)."""
+    arrs = [_f32(a) for a in (cur_rad, prev_rad, prev_pos, prev_nrm)]
+    valid = np.ascontiguousarray(prev_valid, dtype=np.uint8)
+    cp, cn, mo = _f32(cur_pos), _f32(cur_nrm), _f32(motion)
+    N, _, H, W = arrs[0].shape
+    accum = np.empty((N, 3, H, W), dtype=np.float64)
+    mask = np.empty((N, H, W), dtype=np.uint8)
+    _check(_load().kmdo_temporal_accumulate(*[_ptr(a) for a in arrs], _ptr(valid), _ptr(cp), _ptr(cn),
+                                            _ptr(mo), N, H, W, float(pos_tol), float(normal_tol),
+                                            float(alpha), _ptr(accum), _ptr(mask)))
+    return accum, mask

@@ -464,6 +464,68 @@ int kmdo_backward(const float* radiance, const float* importance, const float* b
     return KMDO_OK;
 }
 
+/* ---- temporal accumulation (NEXT row 4) ---------------------------------- */
+int kmdo_temporal_accumulate(const float* cur_rad, const float* prev_rad, const float* prev_pos,
+                             const float* prev_nrm, const uint8_t* prev_valid, const float* cur_pos,
+                             const float* cur_nrm, const float* motion, int32_t N, int32_t H, int32_t W,
+                             float pos_tol, float normal_tol, float alpha, double* accum, uint8_t* mask) {
+    if (N < 0 || H < 0 || W < 0) return KMDO_ERR_DIM;
+    if ((size_t)N * H * W == 0) return KMDO_OK;
+    if (!cur_rad || !prev_rad || !prev_pos || !prev_nrm || !prev_valid || !cur_pos || !cur_nrm || !motion ||
+        !accum || !mask)
+        return KMDO_ERR_NULL;
+    if (!(pos_tol > 0.0f) || !(normal_tol > 0.0f && normal_tol <= 1.0f) || !(alpha > 0.0f && alpha <= 1.0f))
+        return KMDO_ERR_CONFIG;
+    const size_t plane = (size_t)H * W;
+    for (int n = 0; n < N; ++n)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                const size_t p = (size_t)y * W + x;
+                const float* cr = cur_rad + (size_t)n * 3 * plane;
+                /* reproject (nearest pixel, fp32) */
+                const float mx = motion[((size_t)n * 2 + 0) * plane + p];
+                const float my = motion[((size_t)n * 2 + 1) * plane + p];
+                const float fx = floorf(((float)x + mx) + 0.5f);
+                const float fy = floorf(((float)y + my) + 0.5f);
+                int in_bounds = fx >= 0.0f && fx <= (float)(W - 1) && fy >= 0.0f && fy <= (float)(H - 1);
+                size_t s = 0;
+                if (in_bounds) {
+                    s = (size_t)(int)fy * W + (size_t)(int)fx;
+                    in_bounds = prev_valid[(size_t)n * plane + s] != 0;
+                }
+                int m = 0;
+                if (in_bounds) {
+                    /* consistency test (fp32) */
+                    const float* cp = cur_pos + (size_t)n * 3 * plane;
+                    const float* pp = prev_pos + (size_t)n * 3 * plane;
+                    const float* cn = cur_nrm + (size_t)n * 3 * plane;
+                    const float* pn = prev_nrm + (size_t)n * 3 * plane;
+                    float d[3], a[3], b[3];
+                    for (int c = 0; c < 3; ++c) {
+                        d[c] = cp[c * plane + p] - pp[c * plane + s];
+                        a[c] = 2.0f * cn[c * plane + p] - 1.0f;
+                        b[c] = 2.0f * pn[c * plane + s] - 1.0f;
+                    }
+                    const float d2 = (d[0] * d[0] + d[1] * d[1]) + d[2] * d[2];
+                    const float pass_pos = d2 < pos_tol * pos_tol;
+                    const float dot = (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+                    const float aa = (a[0] * a[0] + a[1] * a[1]) + a[2] * a[2];
+                    const float bb = (b[0] * b[0] + b[1] * b[1]) + b[2] * b[2];
+                    const int pass_n = dot > normal_tol * sqrtf(aa * bb);
+                    m = pass_pos && pass_n;
+                }
+                mask[(size_t)n * plane + p] = (uint8_t)m;
+                /* accumulate */
+                for (int c = 0; c < 3; ++c) {
+                    const double cur = cr[c * plane + p];
+                    double v = cur;
+                    if (m) v = (1.0 - (double)alpha) * (double)prev_rad[((size_t)n * 3 + c) * plane + s] + (double)alpha * cur;
+                    accum[((size_t)n * 3 + c) * plane + p] = v;
+                }
+            }
+    return KMDO_OK;
+}
+
 int kmdo_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -114,6 +114,25 @@ int kmdo_backward(const float* radiance, const float* importance, const float* b
                   const int32_t* sizes, int32_t blend_is_logits, double* grad_imp,
                   double* grad_blend);
 
+/* ---- NEXT row 4: temporal accumulation pre-pass (§4.1;
+ * SPEC.md:147-175).  Per pixel p = (x, y) of frame n, in the SPEC's order:
+ *   reproject   s = nearest pixel of (x + mx, y + my), motion = (mx, my) in pixels
+ *               (channel 0 = x); the nearest pixel of v is floor(v + 0.5), taken
+ *               in fp32 as fx = floorf(((float)x + mx) + 0.5f) (reading R21);
+ *               in_bounds = s inside the frame and prev_valid(s) != 0.
+ *   consistency (fp32 decision, reading R22; no FMA contraction):
+ *               d = cur_pos(p) - prev_pos(s);  pass_pos = (d0*d0 + d1*d1) + d2*d2 < pos_tol*pos_tol
+ *               a = 2 cur_nrm(p) - 1, b = 2 prev_nrm(s) - 1   ([0,1] -> [-1,1]);
+ *               pass_n = (a0*b0 + a1*b1) + a2*b2 > normal_tol * sqrtf(((a.a) * (b.b)))
+ *   accumulate  mask = in_bounds && pass_pos && pass_n;
+ *               accum = mask ? (1 - alpha) prev_rad(s) + alpha cur_rad(p) : cur_rad(p)   (fp64)
+ * Layout: rad / pos / nrm [N,3,H,W] float, motion [N,2,H,W] float,
+ * prev_valid and mask [N,H,W] uint8, accum [N,3,H,W] double. */
+int kmdo_temporal_accumulate(const float* cur_rad, const float* prev_rad, const float* prev_pos,
+                             const float* prev_nrm, const uint8_t* prev_valid, const float* cur_pos,
+                             const float* cur_nrm, const float* motion, int32_t N, int32_t H, int32_t W,
+                             float pos_tol, float normal_tol, float alpha, double* accum, uint8_t* mask);
+
 /* Threads OpenMP would use for threads <= 0 (reported as cpu_baseline.cores). */
 int kmdo_max_threads(void);
 

@@ -156,3 +156,63 @@ def make_mr_inputs(N: int, H: int, W: int, sizes_per_level=MR_SIZES, seed: int =
                          for _ in range(N)])
         alphas.append(a.contiguous())
     return MRInputs(base.radiance, imps, blends, alphas)
+
+
+@dataclass
+class TemporalInputs:
+    cur_rad: torch.Tensor     # [N,3,H,W] 1-spp radiance of the current frame
+    prev_rad: torch.Tensor    # [N,3,H,W] accumulated radiance of the previous frame
+    prev_pos: torch.Tensor    # [N,3,H,W] world positions (scene units)
+    prev_nrm: torch.Tensor    # [N,3,H,W] shading normals scaled to [0,1]
+    prev_valid: torch.Tensor  # [N,H,W] uint8
+    cur_pos: torch.Tensor
+    cur_nrm: torch.Tensor
+    motion: torch.Tensor      # [N,2,H,W] pixels, channel 0 = x
+    pos_tol: float            # 1% of the scene's bounding-box diagonal (SPEC.md DESIGN DECISIONS)
+
+
+def _scene(u: torch.Tensor, v: torch.Tensor, ph: torch.Tensor):
+    """World position and [0,1]-scaled normal of a height-field scene z(u, v)
+    seen by an orthographic camera (1 scene unit per pixel)."""
+    z = 40.0 + 6.0 * torch.sin(u / 37.0 + ph[0]) * torch.cos(v / 53.0 + ph[1]) + 3.0 * torch.sin((u + v) / 19.0 + ph[2])
+    dzdu = (6.0 / 37.0) * torch.cos(u / 37.0 + ph[0]) * torch.cos(v / 53.0 + ph[1]) + (3.0 / 19.0) * torch.cos((u + v) / 19.0 + ph[2])
+    dzdv = -(6.0 / 53.0) * torch.sin(u / 37.0 + ph[0]) * torch.sin(v / 53.0 + ph[1]) + (3.0 / 19.0) * torch.cos((u + v) / 19.0 + ph[2])
+    n = torch.stack([-dzdu, -dzdv, torch.ones_like(z)])
+    n = n / n.norm(dim=0, keepdim=True)
+    return torch.stack([u, v, z]), 0.5 * n + 0.5
+
+
+def make_temporal_inputs(N: int, H: int, W: int, seed: int = BASE_SEED + 23, device="cpu") -> TemporalInputs:
+    """NEXT row 4 inputs: a height-field scene under a camera pan of (m0x, m0y)
+    pixels per frame plus sub-pixel smooth jitter in the motion vectors; 3% of
+    the pixels are disoccluded (current geometry displaced far from the previous
+    frame's), 2% have a flipped normal, 0.5% of the history is invalid."""
+    device = torch.device(device)
+    out = {k: [] for k in ("cur_rad", "prev_rad", "prev_pos", "prev_nrm", "prev_valid", "cur_pos", "cur_nrm",
+                           "motion")}
+    for f in range(N):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed + f)
+        ph = torch.rand(3, generator=g, device=device) * 6.283
+        m0 = (torch.rand(2, generator=g, device=device) * 2 - 1) * 4.0
+        yy, xx = torch.meshgrid(torch.arange(H, device=device, dtype=torch.float32),
+                                torch.arange(W, device=device, dtype=torch.float32), indexing="ij")
+        # the previous frame saw scene point (x' - m0x, y' - m0y) at pixel (x', y')
+        prev_pos, prev_nrm = _scene(xx - m0[0], yy - m0[1], ph)
+        # pixel p of the current frame shows the point the previous frame had at
+        # p + m0, i.e. scene point p
+        cur_pos, cur_nrm = _scene(xx, yy, ph)
+        motion = m0.view(2, 1, 1) + 0.3 * _smooth(g, 2, H, W, device)
+        dis = torch.rand((1, H, W), generator=g, device=device) < 0.03
+        cur_pos = torch.where(dis, cur_pos + torch.tensor([0.0, 0.0, 25.0], device=device).view(3, 1, 1), cur_pos)
+        flip = torch.rand((1, H, W), generator=g, device=device) < 0.02
+        cur_nrm = torch.where(flip, 1.0 - cur_nrm, cur_nrm)
+        valid = (torch.rand((H, W), generator=g, device=device) >= 0.005).to(torch.uint8)
+        L = torch.exp(0.75 * _smooth(g, 3, H, W, device))
+        cur_rad = L * torch.empty((3, H, W), device=device).exponential_(1.0, generator=g)
+        prev_rad = L * (1.0 + 0.2 * torch.randn((3, H, W), generator=g, device=device)).clamp_min(0.0)
+        for k, v in (("cur_rad", cur_rad), ("prev_rad", prev_rad), ("prev_pos", prev_pos), ("prev_nrm", prev_nrm),
+                     ("prev_valid", valid), ("cur_pos", cur_pos), ("cur_nrm", cur_nrm), ("motion", motion)):
+            out[k].append(v.contiguous())
+    diag = float((W * W + H * H + 20.0 ** 2) ** 0.5)
+    return TemporalInputs(**{k: torch.stack(v).contiguous() for k, v in out.items()}, pos_tol=0.01 * diag)

@@ -483,3 +483,140 @@ def test_backward_invariants(oracle_mod):
     assert np.abs(gI0).max() < 1e-14 and np.abs(gB0).max() < 1e-14
     gI1, gB1 = oracle_mod.backward(rad, imp, blend, np.zeros_like(G), sizes)
     assert np.all(gI1 == 0) and np.all(gB1 == 0)
+
+
+# ------------------------------------------ temporal accumulation (NEXT row 4)
+def _temporal_case(rng, H=7, W=9, N=1):
+    rad = rng.exponential(1.0, size=(N, 3, H, W)).astype(np.float32)
+    prev = rng.exponential(1.0, size=(N, 3, H, W)).astype(np.float32)
+    pos = (10 * rng.standard_normal((N, 3, H, W))).astype(np.float32)
+    nrm = rng.uniform(0, 1, size=(N, 3, H, W)).astype(np.float32)
+    valid = np.ones((N, H, W), np.uint8)
+    motion = np.zeros((N, 2, H, W), np.float32)
+    return rad, prev, pos, nrm, valid, motion
+
+
+def test_temporal_zero_motion_identical_geometry(oracle_mod):
+    # SPEC.md:152-153 (identity warp) and :160 (identical geometry passes):
+    # accum = (1 - a) prev + a cur everywhere
+    rng = np.random.default_rng(41)
+    rad, prev, pos, nrm, valid, motion = _temporal_case(rng)
+    nrm = np.where(np.abs(2 * nrm - 1).sum(axis=1, keepdims=True) < 0.2, 0.9, nrm).astype(np.float32)
+    acc, mask = oracle_mod.temporal_accumulate(rad, prev, pos, nrm, valid, pos, nrm, motion, pos_tol=0.5,
+                                               normal_tol=0.9, alpha=0.25)
+    assert mask.all()
+    np.testing.assert_allclose(acc, 0.75 * prev.astype(np.float64) + 0.25 * rad, rtol=1e-15)
+
+
+def test_temporal_out_of_bounds_keeps_current_exactly(oracle_mod):
+    # SPEC.md:154 motion (+W, 0) -> mask all false; §4.1 "failed pixels
+    # remain original 1 spp": accum == cur bit for bit; NaN motion likewise
+    rng = np.random.default_rng(42)
+    rad, prev, pos, nrm, valid, motion = _temporal_case(rng)
+    motion[:, 0] = rad.shape[3]
+    acc, mask = oracle_mod.temporal_accumulate(rad, prev, pos, nrm, valid, pos, nrm, motion, pos_tol=1e3)
+    assert not mask.any() and np.array_equal(acc, rad.astype(np.float64))
+    motion[:, 0] = np.nan
+    acc, mask = oracle_mod.temporal_accumulate(rad, prev, pos, nrm, valid, pos, nrm, motion, pos_tol=1e3)
+    assert not mask.any() and np.array_equal(acc, rad.astype(np.float64))
+
+
+def test_temporal_integer_shift(oracle_mod):
+    # shift (1, 0): warped(i, j) = prev(i, j+1) where in bounds.
+    # With cur = 0 the accumulation is (1 - a) warped, so warped is read back.
+    rng = np.random.default_rng(43)
+    rad, prev, pos, nrm, valid, motion = _temporal_case(rng, H=6, W=8)
+    motion[:, 0] = 1.0
+    cur = np.zeros_like(rad)
+    acc, mask = oracle_mod.temporal_accumulate(cur, prev, pos, nrm, valid, pos, nrm, motion, pos_tol=1e6,
+                                               normal_tol=1e-6, alpha=0.5)
+    # geometry test uses prev(i, j+1) vs cur(i, j): disable it with huge tolerances,
+    # except normals: compare only where the shifted normals pass
+    W = rad.shape[3]
+    assert not mask[..., W - 1].any()
+    sel = mask[..., : W - 1].astype(bool)
+    assert sel.any()
+    warped = acc[:, :, :, : W - 1] / 0.5
+    ref = prev[:, :, :, 1:].astype(np.float64)
+    np.testing.assert_array_equal(warped[np.broadcast_to(sel[:, None], warped.shape)],
+                                  ref[np.broadcast_to(sel[:, None], ref.shape)])
+
+
+def test_temporal_nearest_rounding(oracle_mod):
+    # nearest pixel of x + m is floor(x + m + 0.5) (reading R21): m = 0.49 stays,
+    # m = 0.5 moves, m = -0.5 stays, m = -0.51 moves
+    rng = np.random.default_rng(44)
+    rad, prev, pos, nrm, valid, motion = _temporal_case(rng, H=3, W=5)
+    cur = np.zeros_like(rad)
+    for m, shift in ((0.49, 0), (0.5, 1), (-0.5, 0), (-0.51, -1)):
+        motion[:, 0] = m
+        acc, mask = oracle_mod.temporal_accumulate(cur, prev, pos, nrm, valid, pos, nrm, motion, pos_tol=1e6,
+                                                   normal_tol=1e-6, alpha=0.5)
+        j = 2
+        if mask[0, 1, j]:
+            assert acc[0, 0, 1, j] == 0.5 * prev[0, 0, 1, j + shift]
+
+
+def test_temporal_consistency_thresholds(oracle_mod):
+    # displaced positions (10 x tol) fail; flipped normals fail;
+    # invalid history fails; blend arithmetic 0.2: warped 1, cur 0 -> 0.8
+    H, W = 4, 5
+    one = np.ones((1, 3, H, W), np.float32)
+    pos = np.zeros((1, 3, H, W), np.float32)
+    nrm = np.full((1, 3, H, W), 1.0, np.float32)   # (1,1,1) after un-scaling
+    valid = np.ones((1, H, W), np.uint8)
+    motion = np.zeros((1, 2, H, W), np.float32)
+    acc, mask = oracle_mod.temporal_accumulate(0 * one, one, pos, nrm, valid, pos, nrm, motion, pos_tol=0.1,
+                                               alpha=0.2)
+    assert mask.all()
+    np.testing.assert_allclose(acc, 0.8, rtol=1e-7)  # alpha is the fp32 value of 0.2
+    far = pos.copy(); far[:, 2] = 1.0
+    _, mask = oracle_mod.temporal_accumulate(0 * one, one, pos, nrm, valid, far, nrm, motion, pos_tol=0.1)
+    assert not mask.any()
+    _, mask = oracle_mod.temporal_accumulate(0 * one, one, pos, nrm, valid, pos, 1 - nrm, motion, pos_tol=0.1)
+    assert not mask.any()
+    v2 = valid.copy(); v2[0, 1, 2] = 0
+    _, mask = oracle_mod.temporal_accumulate(0 * one, one, pos, nrm, v2, pos, nrm, motion, pos_tol=0.1)
+    assert mask.sum() == H * W - 1 and mask[0, 1, 2] == 0
+
+
+def test_temporal_alpha_one_is_identity_and_mask_matches_predicates(oracle_mod):
+    # SPEC.md invariants: alpha = 1 -> output = cur regardless of the mask;
+    # random buffers: mask equals a direct float32 evaluation of both predicates
+    rng = np.random.default_rng(45)
+    rad, prev, pos, nrm, valid, motion = _temporal_case(rng, H=16, W=20)
+    cpos = (pos + rng.standard_normal(pos.shape).astype(np.float32)).astype(np.float32)
+    cnrm = np.clip(nrm + 0.3 * rng.standard_normal(nrm.shape), 0, 1).astype(np.float32)
+    acc, mask = oracle_mod.temporal_accumulate(rad, prev, pos, nrm, valid, cpos, cnrm, motion, pos_tol=1.5,
+                                               normal_tol=0.8, alpha=1.0)
+    assert np.array_equal(acc, rad.astype(np.float64))
+    f = np.float32
+    d = (cpos - pos).astype(f)
+    d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+    a = (f(2) * cnrm - f(1)).astype(f)
+    b = (f(2) * nrm - f(1)).astype(f)
+    dot = (a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1]) + a[:, 2] * b[:, 2]
+    aa = (a[:, 0] * a[:, 0] + a[:, 1] * a[:, 1]) + a[:, 2] * a[:, 2]
+    bb = (b[:, 0] * b[:, 0] + b[:, 1] * b[:, 1]) + b[:, 2] * b[:, 2]
+    ref = (d2 < f(1.5) * f(1.5)) & (dot > f(0.8) * np.sqrt(aa * bb))
+    assert 0.05 < ref.mean() < 0.95
+    assert np.array_equal(mask.astype(bool), ref)
+
+
+def test_temporal_reduces_variance_static_scene(oracle_mod):
+    # SPEC.md:172 property: static scene, constant signal c with zero-mean
+    # noise; after n accumulated frames the variance is below the input's
+    # (EMA with alpha 0.2: asymptotically alpha / (2 - alpha) = 0.11 of it)
+    rng = np.random.default_rng(46)
+    H, W, c = 48, 48, 2.0
+    pos = np.zeros((1, 3, H, W), np.float32)
+    nrm = np.full((1, 3, H, W), 0.9, np.float32)
+    valid = np.ones((1, H, W), np.uint8)
+    motion = np.zeros((1, 2, H, W), np.float32)
+    acc = (c + rng.standard_normal((1, 3, H, W))).astype(np.float32)
+    for _ in range(30):
+        cur = (c + rng.standard_normal((1, 3, H, W))).astype(np.float32)
+        acc, _ = oracle_mod.temporal_accumulate(cur, acc.astype(np.float32), pos, nrm, valid, pos, nrm, motion,
+                                                pos_tol=0.1, alpha=0.2)
+    v = acc.var()
+    assert v < 0.2 and abs(acc.mean() - c) < 0.05
