@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
-    ap.add_argument("--mode", choices=["frame", "band", "mr", "bwd"], default="frame",
+    ap.add_argument("--mode", choices=["frame", "band", "mr", "bwd", "temporal"], default="frame",
                     help="frame: one frame per rank per step (weak scaling, default); band: ONE "
                          "frame split into row bands across ranks with an NCCL halo exchange "
                          "every step (strong scaling, BASELINE.json configs[3], default 4K)")
@@ -580,6 +580,66 @@ def run_bwd(args, rank, world, local):
         flush=True)
 
 
+def run_temporal(args, rank, world, local):
+    """NEXT row 4: the temporal accumulation pre-pass (reproject + consistency +
+    accumulate) on a 1080p frame per rank per step (weak scaling)."""
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    H, W = args.height, args.width
+    K, Wm, F = args.steps, args.warmup, 4
+    frames = [gen.make_temporal_inputs(1, H, W, seed=gen.BASE_SEED + 23 + 97 * (rank * F + f), device=dev)
+              for f in range(F)]
+    accs = [torch.empty((1, 3, H, W), device=dev) for _ in range(F)]
+    masks = [torch.empty((1, H, W), device=dev, dtype=torch.uint8) for _ in range(F)]
+
+    def step(s):
+        t = frames[s % F]
+        kmd.temporal_accumulate(t.cur_rad, t.prev_rad, t.prev_pos, t.prev_nrm, t.prev_valid, t.cur_pos,
+                                t.cur_nrm, t.motion, t.pos_tol, accum=accs[s % F], mask=masks[s % F])
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for j in range(2 * F):
+            step(j)
+    reps = max(1, K // (2 * F))
+    g.replay()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    steps = reps * 2 * F
+    el = max_over_ranks(a.elapsed_time(b), world)
+    if rank != 0:
+        return
+    # current radiance / position / normal 36, motion 8, previous radiance /
+    # position / normal 36 + validity 1 (gathered), accum 12 + mask 1
+    algo = H * W * 94
+    ms = el / steps
+    peak = measured_peak_hbm()[0]
+    mask_rate = float(masks[0].float().mean())
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s (temporal accumulation pre-pass)",
+        "value": H * W * steps * world / (el / 1e3) / 1e6,
+        "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": Wm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{W}x{H} reproject + consistency + EMA (NEXT row 4)",
+                                        "history_kept": round(mask_rate, 3),
+                                        "l2": f"{F} resident frames of 94 B/px rotate ({F * H * W * 94 / 1e6:.0f} MB > 126 MB L2)"},
+        "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": algo / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo},
+        "clocks": clk.summary(), "gpu_launches": steps}), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup()
@@ -592,6 +652,8 @@ def main():
             run_mr(args, rank, world, local)
         elif args.mode == "bwd":
             run_bwd(args, rank, world, local)
+        elif args.mode == "temporal":
+            run_temporal(args, rank, world, local)
         else:
             run_kmd(args, rank, world, local)
     finally:

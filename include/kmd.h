@@ -214,6 +214,31 @@ kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* i
                                            void* workspace, size_t workspace_bytes,
                                            kmd_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT row 4: the temporal accumulation pre-pass (§4.1;
+ * SPEC.md:147-175), fused into one pass over [N,H,W] pixels:
+ *   reproject    s = nearest pixel of p + motion(p): fx = floorf(((float)x + mx) + 0.5f),
+ *                likewise fy (reading R21); in bounds iff s lies in the frame
+ *                and prev_valid(s) != 0;
+ *   consistency  fp32, this exact order, no FMA contraction (reading R22):
+ *                d = cur_position(p) - prev_position(s),
+ *                (d0*d0 + d1*d1) + d2*d2 < pos_tol*pos_tol, and with a = 2 cur_normal(p) - 1,
+ *                b = 2 prev_normal(s) - 1 (normals stored in [0,1]):
+ *                (a0*b0 + a1*b1) + a2*b2 > normal_tol * sqrtf(((a.a) * (b.b)));
+ *   accumulate   accum = mask ? (1 - alpha) prev_radiance(s) + alpha cur_radiance(p)
+ *                             : cur_radiance(p)   ("failed pixels remain original 1 spp").
+ * Device buffers: radiance / position / normal [N,3,H,W] float, motion
+ * [N,2,H,W] float (pixels; channel 0 = x), prev_valid [N,H,W] uint8, accum
+ * [N,3,H,W] float, mask [N,H,W] uint8 or NULL.  accum may alias cur_radiance;
+ * it must not overlap any prev_* buffer (KMD_ERR_ALIAS).  pos_tol > 0,
+ * normal_tol in (0, 1], alpha in (0, 1], else KMD_ERR_CONFIG.               */
+kmd_status kmd_temporal_accumulate(const float* cur_radiance, const float* prev_radiance,
+                                   const float* prev_position, const float* prev_normal,
+                                   const uint8_t* prev_valid, const float* cur_position,
+                                   const float* cur_normal, const float* motion, float* accum,
+                                   uint8_t* mask, int32_t N, int32_t H, int32_t W, float pos_tol,
+                                   float normal_tol, float alpha, kmd_stream_t stream);
+
 /* Algorithmic HBM bytes of one kmd_decode_filter_fuse call:
  * N*H*W*4*(3 + M + (blend? M : 0) + 3)  (inputs read once, output written once). */
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,

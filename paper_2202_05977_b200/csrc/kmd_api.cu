@@ -541,6 +541,35 @@ kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* i
     return e == cudaSuccess ? KMD_OK : cuda_fail(e, "backward launch");
 }
 
+// ---------------------------------------------------------------------------
+// NEXT row 4: temporal accumulation
+kmd_status kmd_temporal_accumulate(const float* cur_radiance, const float* prev_radiance,
+                                   const float* prev_position, const float* prev_normal,
+                                   const uint8_t* prev_valid, const float* cur_position,
+                                   const float* cur_normal, const float* motion, float* accum,
+                                   uint8_t* mask, int32_t N, int32_t H, int32_t W, float pos_tol,
+                                   float normal_tol, float alpha, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0 || (N > 0 && (H < 1 || W < 1))) return fail(KMD_ERR_DIM, "bad N/H/W");
+    if (!(pos_tol > 0.f)) return fail(KMD_ERR_CONFIG, "pos_tol must be > 0");
+    if (!(normal_tol > 0.f && normal_tol <= 1.f)) return fail(KMD_ERR_CONFIG, "normal_tol must be in (0, 1]");
+    if (!(alpha > 0.f && alpha <= 1.f)) return fail(KMD_ERR_CONFIG, "alpha must be in (0, 1]");
+    if (N == 0) return KMD_OK;
+    if (!cur_radiance || !prev_radiance || !prev_position || !prev_normal || !prev_valid || !cur_position ||
+        !cur_normal || !motion || !accum)
+        return fail(KMD_ERR_NULL, "NULL buffer");
+    const size_t b3 = (size_t)N * 3 * H * W * sizeof(float), b1 = (size_t)N * H * W;
+    if (overlaps(accum, b3, prev_radiance, b3) || overlaps(accum, b3, prev_position, b3) ||
+        overlaps(accum, b3, prev_normal, b3) || overlaps(accum, b3, prev_valid, b1) ||
+        (mask && (overlaps(mask, b1, prev_radiance, b3) || overlaps(mask, b1, prev_valid, b1) ||
+                  overlaps(mask, b1, accum, b3))))
+        return fail(KMD_ERR_ALIAS, "accum / mask overlap a previous-frame buffer");
+    cudaError_t e = kmd::launch_temporal(cur_radiance, prev_radiance, prev_position, prev_normal, prev_valid,
+                                         cur_position, cur_normal, motion, accum, mask, N, H, W, pos_tol,
+                                         normal_tol, alpha, (cudaStream_t)stream);
+    return e == cudaSuccess ? KMD_OK : cuda_fail(e, "temporal launch");
+}
+
 int64_t kmd_algorithmic_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
                               int32_t has_blend) {
     if (!cfg || N < 0 || H < 0 || W < 0) return -1;

@@ -34,4 +34,10 @@ cudaError_t launch_backward(const float* rad, const float* imp, const float* ble
                             float* gB, int N, int H, int W, int M, const int* sizes, int logits, float* ws,
                             cudaStream_t st);
 
+// temporal accumulation pre-pass (NEXT row 4; kmd_temporal.cu)
+cudaError_t launch_temporal(const float* cur_rad, const float* prev_rad, const float* prev_pos,
+                            const float* prev_nrm, const unsigned char* prev_valid, const float* cur_pos,
+                            const float* cur_nrm, const float* motion, float* accum, unsigned char* mask, int N,
+                            int H, int W, float pos_tol, float normal_tol, float alpha, cudaStream_t st);
+
 }  // namespace kmd

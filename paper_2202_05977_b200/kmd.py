@@ -69,7 +69,7 @@ _lib = None
 EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
            "kmd_mr_workspace_bytes", "kmd_mr_decode_filter_fuse", "kmd_downsample2x2",
            "kmd_combine_resolutions", "kmd_backward_workspace_bytes",
-           "kmd_decode_filter_fuse_backward",
+           "kmd_decode_filter_fuse_backward", "kmd_temporal_accumulate",
            "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
            "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
@@ -101,6 +101,8 @@ def lib(build_if_missing: bool = True):
     L.kmd_downsample2x2.argtypes = [P, P, i32, i32, i32, i32, P]
     L.kmd_combine_resolutions.argtypes = [P, P, P, P, i32, i32, i32, P]
     L.kmd_fuse.argtypes = [P, P, P, i32, i32, i32, i32, i32, P]
+    f32 = ctypes.c_float
+    L.kmd_temporal_accumulate.argtypes = [P, P, P, P, P, P, P, P, P, P, i32, i32, i32, f32, f32, f32, P]
     L.kmd_backward_workspace_bytes.argtypes = [i32, i32, i32, C]
     L.kmd_backward_workspace_bytes.restype = ctypes.c_size_t
     L.kmd_decode_filter_fuse_backward.argtypes = [P, P, P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
@@ -119,6 +121,7 @@ def lib(build_if_missing: bool = True):
     for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
               "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
               "kmd_downsample2x2", "kmd_combine_resolutions", "kmd_decode_filter_fuse_backward",
+              "kmd_temporal_accumulate",
               "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -438,3 +441,37 @@ class DecodeFilterFuse(torch.autograd.Function):
         gI, gB = decode_filter_fuse_backward(radiance, importance, blend, grad_out.contiguous(),
                                              ctx.sizes, ctx.logits)
         return None, gI, gB, None, None
+
+
+# ------------------------------------------------ temporal accumulation (NEXT row 4)
+def temporal_accumulate(cur_rad: torch.Tensor, prev_rad: torch.Tensor, prev_pos: torch.Tensor,
+                        prev_nrm: torch.Tensor, prev_valid: torch.Tensor, cur_pos: torch.Tensor,
+                        cur_nrm: torch.Tensor, motion: torch.Tensor, pos_tol: float,
+                        normal_tol: float = 0.9, alpha: float = 0.2,
+                        accum: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None,
+                        want_mask: bool = True, stream: Optional[torch.cuda.Stream] = None):
+    """Reproject + consistency test + accumulate (§4.1)
+    in one kernel: returns (accum [N,3,H,W] fp32, mask [N,H,W] uint8 or None)."""
+    N, _, H, W = cur_rad.shape
+    ptrs = [_dev_f32(nm, t, (N, 3, H, W)) for nm, t in (("cur_rad", cur_rad), ("prev_rad", prev_rad),
+                                                        ("prev_pos", prev_pos), ("prev_nrm", prev_nrm))]
+    if prev_valid.dtype != torch.uint8 or prev_valid.device.type != "cuda" or not prev_valid.is_contiguous() \
+            or tuple(prev_valid.shape) != (N, H, W):
+        raise ValueError("prev_valid must be a contiguous CUDA uint8 tensor [N,H,W]")
+    cp = _dev_f32("cur_pos", cur_pos, (N, 3, H, W))
+    cn = _dev_f32("cur_nrm", cur_nrm, (N, 3, H, W))
+    mo = _dev_f32("motion", motion, (N, 2, H, W))
+    if accum is None:
+        accum = torch.empty((N, 3, H, W), device=cur_rad.device, dtype=torch.float32)
+    ap = _dev_f32("accum", accum, (N, 3, H, W))
+    mp = None
+    if want_mask:
+        if mask is None:
+            mask = torch.empty((N, H, W), device=cur_rad.device, dtype=torch.uint8)
+        if mask.dtype != torch.uint8 or tuple(mask.shape) != (N, H, W) or not mask.is_contiguous():
+            raise ValueError("mask must be a contiguous uint8 tensor [N,H,W]")
+        mp = mask.data_ptr()
+    _check(lib().kmd_temporal_accumulate(*ptrs, prev_valid.data_ptr(), cp, cn, mo, ap, mp, N, H, W,
+                                         float(pos_tol), float(normal_tol), float(alpha),
+                                         _stream(cur_rad, stream)))
+    return accum, (mask if want_mask else None)
