@@ -48,7 +48,10 @@ namespace tma {
 constexpr int RMAX = 6;
 constexpr int TW = 52;              // output columns per tile
 constexpr int FW = TW + 2 * RMAX;   // 64 field columns (2 warps), global x0-6 .. x0+57
-constexpr int TH = 24;              // output rows per tile
+#ifndef KMD_TH
+#define KMD_TH 27
+#endif
+constexpr int TH = KMD_TH;          // output rows per tile
 constexpr int FH = TH + 2 * RMAX;   // 36 field rows in every box
 // Every TMA box starts at column x0-8: the innermost box coordinate must be a
 // multiple of 16 bytes when it is negative (measured on this B200: -6 faults,
@@ -58,11 +61,11 @@ constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> confli
 constexpr int VS = 68;
 constexpr int SEG = 7;              // pixels per fusion thread (segments of 7/6 alternate)
 constexpr int NSEG = 8;             // segments per output row: 52 = 4 x (7 + 6)
-constexpr int NI = 4;               // input (importance) ring depth
+constexpr int NI = TH > 24 ? 3 : 4; // input (importance) ring depth
 constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
 constexpr int NV = 3;               // V ring depth (field -> fusion)
 constexpr int NFIELD = 4;           // field warps
-constexpr int NFUSE = 6;            // fusion warps (TH * NSEG = 192 threads)
+constexpr int NFUSE = (TH * NSEG + 31) / 32;  // fusion warps (one thread per (row, segment))
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 constexpr float L2E_LO = 1.925963033500011079e-08f;       // log2(e) - L2E
@@ -71,7 +74,7 @@ constexpr float LN2 = 0.693147180559945309f;
 struct InSlot {
     alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
 };
-struct Slot {
+struct alignas(128) Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
 };
 // blend box: the 52 output columns plus 4 of padding, starting at x0 (no
@@ -485,6 +488,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // LDS.128 of V.  Every thread computes 7 pixels (the 7th of a 6-pixel
         // segment is recomputed by its neighbour and not stored).
         const int ty = c / NSEG, sub = c % NSEG;
+        const bool active = ty < TH;  // the last fusion warp may have spare lanes
         const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
         const int len = (0x76677766u >> (4 * sub)) & 0xf;
         int vs = 0, vph = 0, bs = 0, bph = 0;  // V / blend ring slot and phase of the current step
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // albedo of this thread's pixels, loaded now so the latency hides
             // behind the M sizes (remodulation epilogue)
             float alb[SEG][3];
-            if (SP::ALB && p.albedo) {
+            if (SP::ALB && p.albedo && active) {
                 const size_t op = (size_t)p.out_rows * p.W;
                 const int gyc = clampi(tc.y0 + ty - p.out_y0, 0, p.out_rows - 1);
                 const float* ab = p.albedo + (size_t)tc.n * 3 * op + (size_t)gyc * p.W;
@@ -516,7 +520,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < M; ++i) {
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                if (!(p.debug & 64)) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, (rpack >> (4 * i)) & 15);
+                if (!(p.debug & 64) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, (rpack >> (4 * i)) & 15);
                 __syncwarp();
                 if ((c & 31) == 0) {
                     mbar_arrive(&sm.v_empty[vs]);
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const bool b = !(st.dmin[j] >= 1e-30f) || (norm && !(st.S[j] >= 1e-30f && st.S[j] <= 1e30f)) ||
                                !(fabsf(o0) + fabsf(o1) + fabsf(o2) <= 3.0e38f);
                 bad |= b ? (1u << j) : 0u;
-                if (j < len) {
+                if (j < len && active) {
                     float r0 = o0, r1 = o1, r2 = o2;
                     if (SP::ALB && p.albedo) {
                         r0 *= alb[j][0];
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             // rare: pixels outside the unshifted exp range -> exact evaluation
-            if (bad && row_ok && !(p.debug & 2)) {
+            if (bad && row_ok && active && !(p.debug & 2)) {
                 for (int j = 0; j < len; ++j) {
                     const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
