@@ -68,8 +68,6 @@ constexpr int NFIELD = 4;           // field warps
 constexpr int NFUSE = (TH * NSEG + 31) / 32;  // fusion warps (one thread per (row, segment))
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
-constexpr float L2E_LO = 1.925963033500011079e-08f;       // log2(e) - L2E
-constexpr float LN2 = 0.693147180559945309f;
 
 struct InSlot {
     alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
@@ -135,14 +133,16 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
 
-// exp(x) = 2^(x log2 e) with the product's rounding error carried to first
-// order: t = fl(x L2E), c = (x L2E - t) + x L2E_LO, e = 2^t (1 + c ln 2).
-// ~2-3 ulp for |x| <= 88 (MUFU.EX2 + 5 FP32 ops).
+// exp(x) = 2^t (1 + r) with t = fl(x log2 e) and r = x - t ln 2 the exact
+// remainder (two-constant Cody-Waite: the FMAs cancel exactly), to first
+// order in |r| <= 2^-24 |t| ln 2: ~2-3 ulp for |x| <= 88, MUFU.EX2 + 4 FP32 ops.
+constexpr float LN2_HI = 0.693147182464599609375f;           // fl(ln 2)
+constexpr float LN2_LO = -1.904654299957768e-09f;            // ln 2 - LN2_HI
 __device__ __forceinline__ float exp_acc(float x) {
     const float t = x * L2E;
-    const float c = fmaf(x, L2E_LO, fmaf(x, L2E, -t));
+    const float r = fmaf(-t, LN2_LO, fmaf(-t, LN2_HI, x));
     const float e = ex2_approx(t);
-    return fmaf(e * c, LN2, e);
+    return fmaf(e, r, e);
 }
 
 // Gil-Werman line sums (gw_line, gw_line_field): kmd_gw.cuh
