@@ -13,41 +13,69 @@
 namespace kmd {
 namespace {
 
-// out[n][c][y][x] = 0.25 * (in[2y][2x] + in[2y][2x+1] + in[2y+1][2x] + in[2y+1][2x+1])
+// out[n][c][y][x] = 0.25 * ((in[2y][2x] + in[2y][2x+1]) + (in[2y+1][2x] + in[2y+1][2x+1]))
+// One thread per two horizontally adjacent outputs: two 16-byte loads per
+// input row when the input row is 16-byte aligned (Wi % 4 == 0), else scalar.
 __global__ void __launch_bounds__(256) down2_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     long long planes, int Ho, int Wo) {
-    const long long total = planes * Ho * Wo;
-    const int Wi = 2 * Wo;
+    const int Wi = 2 * Wo, wp = (Wo + 1) / 2;
+    const long long total = planes * Ho * wp;
+    const bool vec = (Wi % 4) == 0 && ((uintptr_t)in & 15) == 0;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
-        const long long pl = t / ((long long)Ho * Wo);
-        const int r = (int)(t - pl * Ho * Wo), y = r / Wo, x = r - y * Wo;
+        const long long pl = t / ((long long)Ho * wp);
+        const int r = (int)(t - pl * Ho * wp), y = r / wp, x = 2 * (r - y * wp);
         const float* s = in + (pl * 2 * Ho + 2 * y) * (long long)Wi + 2 * x;
-        const float a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + Wi), d = __ldg(s + Wi + 1);
-        out[t] = 0.25f * ((a + b) + (c + d));
+        float* o = out + (pl * Ho + y) * (long long)Wo + x;
+        if (vec && x + 1 < Wo) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(s));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(s + Wi));
+            o[0] = 0.25f * ((a.x + a.y) + (b.x + b.y));
+            o[1] = 0.25f * ((a.z + a.w) + (b.z + b.w));
+        } else {
+            for (int j = 0; j < 2 && x + j < Wo; ++j) {
+                const float* q = s + 2 * j;
+                o[j] = 0.25f * ((__ldg(q) + __ldg(q + 1)) + (__ldg(q + Wi) + __ldg(q + Wi + 1)));
+            }
+        }
     }
 }
 
-// Eq. 7: o = f - alpha * [U D f] + alpha * [U c]
+// Eq. 7: o = f - alpha * [U D f] + alpha * [U c], computed as
+// fma(alpha, Uc - UDf, f).  One thread per 2x2 block of fine pixels and all
+// three channels: the block's D f, the one coarse value and the 2x2 alphas are
+// each read once (8-byte vectors when W is even).
+template <bool VEC>
 __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ fine, const float* __restrict__ coarse,
                                                       const float* __restrict__ alpha, float* __restrict__ out,
                                                       int N, int H, int W) {
-    const long long total = (long long)N * 3 * H * W;
     const int Hc = H / 2, Wc = W / 2;
+    const long long total = (long long)N * Hc * Wc;
+    const size_t plane = (size_t)H * W, cplane = (size_t)Hc * Wc;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
-        const long long plane = t / ((long long)H * W);  // n*3 + c
-        const int r = (int)(t - plane * H * W), y = r / W, x = r - y * W;
-        const long long n = plane / 3;
-        const float* fp = fine + plane * H * W;
-        const int y0 = y & ~1, x0 = x & ~1;
-        const float a = __ldg(fp + (long long)y0 * W + x0), b = __ldg(fp + (long long)y0 * W + x0 + 1);
-        const float c = __ldg(fp + (long long)(y0 + 1) * W + x0), d = __ldg(fp + (long long)(y0 + 1) * W + x0 + 1);
-        const float udf = 0.25f * ((a + b) + (c + d));
-        const float uc = __ldg(coarse + plane * Hc * Wc + (long long)(y >> 1) * Wc + (x >> 1));
-        const float al = __ldg(alpha + n * H * W + (long long)y * W + x);
-        const float f = __ldg(fp + (long long)y * W + x);
-        out[t] = fmaf(al, uc - udf, f);
+        const int n = (int)(t / ((long long)Hc * Wc));
+        const int r = (int)(t - (long long)n * Hc * Wc), yc = r / Wc, xc = r - yc * Wc;
+        const size_t p0 = (size_t)(2 * yc) * W + 2 * xc;
+        const float* al = alpha + (size_t)n * plane + p0;
+        auto ld2 = [](const float* q) {
+            return VEC ? __ldg(reinterpret_cast<const float2*>(q)) : make_float2(__ldg(q), __ldg(q + 1));
+        };
+        auto st2 = [](float* q, float2 v) {
+            if (VEC) *reinterpret_cast<float2*>(q) = v;
+            else q[0] = v.x, q[1] = v.y;
+        };
+        const float2 a0 = ld2(al), a1 = ld2(al + W);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float* fp = fine + ((size_t)n * 3 + c) * plane + p0;
+            const float2 f0 = ld2(fp), f1 = ld2(fp + W);
+            const float udf = 0.25f * ((f0.x + f0.y) + (f1.x + f1.y));
+            const float d = __ldg(coarse + ((size_t)n * 3 + c) * cplane + (size_t)yc * Wc + xc) - udf;
+            float* op = out + ((size_t)n * 3 + c) * plane + p0;
+            st2(op, make_float2(fmaf(a0.x, d, f0.x), fmaf(a0.y, d, f0.y)));
+            st2(op + W, make_float2(fmaf(a1.x, d, f1.x), fmaf(a1.y, d, f1.y)));
+        }
     }
 }
 
@@ -63,7 +91,7 @@ int grid_for(long long n) {
 }  // namespace
 
 cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, int Wo, cudaStream_t st) {
-    const long long n = planes * Ho * Wo;
+    const long long n = planes * Ho * ((Wo + 1) / 2);
     if (n == 0) return cudaSuccess;
     down2_kernel<<<grid_for(n), 256, 0, st>>>(in, out, planes, Ho, Wo);
     return cudaGetLastError();
@@ -71,9 +99,11 @@ cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, 
 
 cudaError_t launch_combine(const float* fine, const float* coarse, const float* alpha, float* out, int N, int H,
                            int W, cudaStream_t st) {
-    const long long n = (long long)N * 3 * H * W;
+    const long long n = (long long)N * (H / 2) * (W / 2);
     if (n == 0) return cudaSuccess;
-    combine_kernel<<<grid_for(n), 256, 0, st>>>(fine, coarse, alpha, out, N, H, W);
+    const bool vec = (((uintptr_t)fine | (uintptr_t)alpha | (uintptr_t)out) & 7) == 0;
+    if (vec) combine_kernel<true><<<grid_for(n), 256, 0, st>>>(fine, coarse, alpha, out, N, H, W);
+    else combine_kernel<false><<<grid_for(n), 256, 0, st>>>(fine, coarse, alpha, out, N, H, W);
     return cudaGetLastError();
 }
 
