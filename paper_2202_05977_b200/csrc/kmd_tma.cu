@@ -11,20 +11,20 @@
 // non-negative terms (no subtraction, no cancellation), in an order fixed by
 // the window's position in the global tile grid.
 //
-// Per CTA (one per SM), per 52 x 24 output tile, per kernel size i:
-//   warp 0  (TMA)      cp.async.bulk.tensor loads: radiance box [3][36][68]
-//                      (double-buffered per tile) and the I_i box [36][68]
-//                      into a 5-deep input ring (mbarrier expect_tx), running
-//                      ahead of the compute by up to 5 (tile, size) steps.
-//   warps 1-4 (field)  job = (size i, 32-column half): lane = field column;
-//                      e = exp(I) once per field pixel, vertical box sums in
-//                      registers, V[24][64] float4 into a 3-deep V ring; the
-//                      half-0 warp also TMA-loads the blend box [24][68] of
-//                      size i next to its V.
-//   warps 5-7 (fusion) thread = (row, 13-pixel segment): horizontal box sums of
-//                      V, R = num * rcp(den), online softmax over the blend
-//                      logits (Eq. 5); after the last
-//                      size the tile is staged and written by one TMA store.
+// Per CTA (one per SM, 12 warps), per 52 x 27 output tile, per kernel size i:
+//   warp 0  (TMA)        one elected thread issues, in order, the radiance box
+//                        [3][39][68] (per tile, double-buffered), the I_i box
+//                        [39][68] (3-deep ring) and the blend box [27][56]
+//                        (4-deep ring), each with an mbarrier expect_tx.
+//   warps 1-4 (field)    job = (size i, 32-column half): lane = field column;
+//                        e = exp(I) once per field pixel, vertical Gil-Werman
+//                        sums in registers (rolled block loop), V[27][64]
+//                        float4 into a 3-deep V ring.
+//   warps 5-11 (fusion)  thread = (row, 7/6-pixel segment): horizontal sums of
+//                        V, R = num * rcp(den), acc += exp(B_i) R and
+//                        S += exp(B_i) (Eq. 5); after
+//                        the last size Rhat = acc / S is staged and the tile
+//                        leaves with one TMA store.
 // Clamp-to-edge (reading R1): columns via a per-lane clamped smem column;
 // rows outside the frame are replicated into the TMA zero-filled box rows by
 // the field warps of border tiles.  Pixels whose box denominators leave
@@ -48,6 +48,7 @@ namespace tma {
 constexpr int RMAX = 6;
 constexpr int TW = 52;              // output columns per tile
 constexpr int FW = TW + 2 * RMAX;   // 64 field columns (2 warps), global x0-6 .. x0+57
+static_assert(FW == 64, "two 32-lane field halves per size");
 #ifndef KMD_TH
 #define KMD_TH 27
 #endif
