@@ -382,7 +382,7 @@ def run_kmd(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": recorded_traffic(workload),
                      "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src,
-                     "kernel": "fused decode+filter+fuse (libkmd)"},
+                     "kernel": f"fused decode+filter+fuse (libkmd, {kmd.last_kernel()})"},
         "gpu_launches": K * kmd.launches_per_call(),
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -9,6 +9,13 @@
 #include "kmd_kernels.h"
 
 namespace {
+thread_local int g_last_kernel = 0;
+}  // namespace
+namespace kmd {
+void set_last_kernel(int k) { g_last_kernel = k; }
+}  // namespace kmd
+
+namespace {
 
 thread_local char g_err[512] = "";
 
@@ -73,9 +80,16 @@ kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t str
         q.imp = p.imp + (size_t)n0 * p.M * bplane;
         q.blend = p.blend ? p.blend + (size_t)n0 * p.M * oplane : nullptr;
         q.out = p.out + (size_t)n0 * 3 * oplane;
-        cudaError_t e = kmd::tma_supported(q)  ? kmd::launch_fused_tma(q, stream)
-                        : kmd::ws_supported(q) ? kmd::launch_fused_ws(q, stream)
-                                               : kmd::launch_fused_direct(q, stream);
+        cudaError_t e;
+        if (kmd::tma_supported(q)) {
+            e = kmd::launch_fused_tma(q, stream);  // records its specialisation
+        } else if (kmd::ws_supported(q)) {
+            kmd::set_last_kernel(kmd::LK_WS);
+            e = kmd::launch_fused_ws(q, stream);
+        } else {
+            kmd::set_last_kernel(kmd::LK_DIRECT);
+            e = kmd::launch_fused_direct(q, stream);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
     }
     return KMD_OK;
@@ -596,5 +610,7 @@ const char* kmd_status_string(kmd_status s) {
 const char* kmd_last_error(void) { return g_err; }
 
 int32_t kmd_version(void) { return KMD_VERSION_MAJOR * 100 + KMD_VERSION_MINOR; }
+
+int32_t kmd_last_kernel(void) { return g_last_kernel; }
 
 }  // extern "C"

@@ -680,10 +680,17 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     // and without the albedo epilogue, and the multi-resolution levels' M = 2
     const bool softmax = p.blend != nullptr && p.blend_is_logits, alb = p.albedo != nullptr;
     if (!(p.debug & 2048) && softmax) {
-        if (p.M == 6) return alb ? launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, true, 6>>)
-                                 : launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6>>);
-        if (p.M == 2 && !alb) return launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>);
+        if (p.M == 6) {
+            set_last_kernel(alb ? LK_TMA_M6_ALB : LK_TMA_M6);
+            return alb ? launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, true, 6>>)
+                       : launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6>>);
+        }
+        if (p.M == 2 && !alb) {
+            set_last_kernel(LK_TMA_M2);
+            return launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>);
+        }
     }
+    set_last_kernel(LK_TMA);
     return launch(fused_tma_kernel<Runtime>);
 }
 

@@ -73,7 +73,7 @@ EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodu
            "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
            "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
-           "kmd_status_string", "kmd_last_error", "kmd_version")
+           "kmd_status_string", "kmd_last_error", "kmd_version", "kmd_last_kernel")
 
 
 def lib(build_if_missing: bool = True):
@@ -118,6 +118,8 @@ def lib(build_if_missing: bool = True):
     L.kmd_last_error.argtypes = []
     L.kmd_last_error.restype = ctypes.c_char_p
     L.kmd_version.argtypes = []
+    L.kmd_last_kernel.argtypes = []
+    L.kmd_last_kernel.restype = ctypes.c_int32
     for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
               "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
               "kmd_downsample2x2", "kmd_combine_resolutions", "kmd_decode_filter_fuse_backward",
@@ -306,6 +308,15 @@ def algorithmic_bytes(N: int, H: int, W: int, sizes: Sequence[int], has_blend: b
 
 def launches_per_call() -> int:
     return int(lib().kmd_launches_per_call())
+
+
+LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma", 4: "v3-tma-M6", 5: "v3-tma-M6-albedo",
+               6: "v3-tma-M2"}
+
+
+def last_kernel() -> str:
+    """Kernel variant of the last fused launch on this thread (diagnostic)."""
+    return LAST_KERNEL.get(int(lib().kmd_last_kernel()), "?")
 
 
 def version() -> int:

@@ -22,6 +22,8 @@ def test_fused_remodulation_matches_oracle(oracle_mod, cuda_device, H, W, sizes)
                                  None if inp.blend is None else inp.blend.to(dev), sizes,
                                  albedo=alb.to(dev))
     torch.cuda.synchronize()
+    if sizes == PAPER:
+        assert kmd.last_kernel() == "v3-tma-M6-albedo"
     fused = oracle_mod.decode_filter_fuse(inp.radiance.numpy(), inp.importance.numpy(),
                                           None if inp.blend is None else inp.blend.numpy(), sizes)
     ref = oracle_mod.remodulate(fused, alb.numpy())

@@ -54,9 +54,29 @@ def test_config1_720p_paper_set_full_frame(oracle_mod, cuda_device):
     (2, 65, 129, [13, 11, 9, 7, 5, 3]),     # paper set, descending order
 ])
 def test_shapes_fuzz(oracle_mod, cuda_device, N, H, W, sizes):
+    """Mostly W % 4 != 0 / k > 13 shapes: the v2 and v1 kernels."""
     inp = gen.make_inputs(N, H, W, len(sizes), seed=1000 + H * W)
-    assert_parity(_run(inp, sizes, cuda_device), _oracle(oracle_mod, inp, sizes),
-                  what=f"{N}x{H}x{W} {sizes}")
+    out = _run(inp, sizes, cuda_device)
+    assert kmd.last_kernel() == ("v1-direct" if max(sizes) > 13 else ("v2-ws" if W % 4 else "v3-tma-M6"))
+    assert_parity(out, _oracle(oracle_mod, inp, sizes), what=f"{N}x{H}x{W} {sizes}")
+
+
+@pytest.mark.parametrize("N,H,W,sizes", [
+    (1, 61, 108, [3, 5, 7, 9, 11, 13]),     # M = 6 specialisation, ragged 52x27 tiles both ways
+    (1, 27, 52, [3, 5, 7, 9, 11, 13]),      # exactly one tile
+    (2, 30, 56, [3, 5]),                    # M = 2 specialisation (MR levels), N > 1
+    (1, 83, 200, [3, 7, 11]),               # runtime-M kernel
+    (1, 28, 56, [13]),                      # M = 1, the largest TMA window
+    (3, 54, 104, [13, 3, 9, 5, 11, 7]),     # M = 6 specialisation, unsorted sizes, N = 3
+    (1, 13, 16, [13, 13]),                  # H == k: every row is a border row
+])
+def test_tma_kernel_shapes(oracle_mod, cuda_device, N, H, W, sizes):
+    """W % 4 == 0: the TMA kernel (kmd_tma.cu) and its specialisations."""
+    inp = gen.make_inputs(N, H, W, len(sizes), seed=2000 + H * W)
+    out = _run(inp, sizes, cuda_device)
+    expect = {6: "v3-tma-M6", 2: "v3-tma-M2"}.get(len(sizes), "v3-tma")
+    assert kmd.last_kernel() == expect
+    assert_parity(out, _oracle(oracle_mod, inp, sizes), what=f"tma {N}x{H}x{W} {sizes}")
 
 
 @pytest.mark.parametrize("dist", ["uniform40", "spikes", "extreme", "const"])
