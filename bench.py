@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["kmd", "reference"], default="kmd")
-    ap.add_argument("--mode", choices=["frame", "band", "mr", "bwd", "temporal"], default="frame",
+    ap.add_argument("--mode", choices=["frame", "band", "mr", "bwd", "temporal", "sweep", "batch"], default="frame",
                     help="frame: one frame per rank per step (weak scaling, default); band: ONE "
                          "frame split into row bands across ranks with an NCCL halo exchange "
                          "every step (strong scaling, BASELINE.json configs[3], default 4K)")
@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--sizes", type=str, default=",".join(map(str, PAPER_SIZES)))
     ap.add_argument("--rotate", type=int, default=4, help="distinct resident frames per rank")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=256,
+                    help="--mode batch: frames per rank in one launch (BASELINE.json configs[4])")
     ap.add_argument("--albedo", action="store_true",
                     help="NEXT row 1: fuse the albedo remodulation epilogue (out = Rhat * albedo)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -640,6 +642,128 @@ def run_temporal(args, rank, world, local):
         "clocks": clk.summary(), "gpu_launches": steps}), flush=True)
 
 
+def _graph_time_ms(step, n_launch, K, Wm, dev):
+    """Mean ms per launch of `step` (CUDA-graph captured, n_launch per graph)."""
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for j in range(n_launch):
+            step(j)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    reps = max(1, K // n_launch)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize(dev)
+    return a.elapsed_time(b) / (reps * n_launch)
+
+
+def run_sweep(args, rank, world, local):
+    """SURVEY.md §8(d) sweep-M / sweep-k: time per frame vs the number of fused
+    sizes (cumulative {3}, {3,5}, ..., {3..13}: the analogue of the paper's
+    Fig. 10/11) and vs one kernel size k at M = 1
+    (the box-sum kernel is ~flat in k; k > 13 takes the direct v1 kernel)."""
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    H, W, F = args.height, args.width, 3
+    K, Wm = max(64, args.steps // 8), max(3, args.warmup)
+    peak = measured_peak_hbm()[0]
+    rows = []
+    with ClockSampler(local) as clk:
+        for sizes in [PAPER_SIZES[:m] for m in range(1, 7)] + [[k] for k in (3, 5, 9, 13, 21, 31)]:
+            M = len(sizes)
+            inp = gen.make_inputs(F, H, W, M, device=dev, with_blend=M > 1)
+            out = torch.empty((F, 3, H, W), device=dev)
+
+            def step(s, inp=inp, out=out, sizes=sizes):
+                f = s % F
+                kmd.decode_filter_fuse(inp.radiance[f:f + 1], inp.importance[f:f + 1],
+                                       None if inp.blend is None else inp.blend[f:f + 1], sizes,
+                                       out=out[f:f + 1])
+            ms = _graph_time_ms(step, 2 * F, K, Wm, dev)
+            algo = kmd.algorithmic_bytes(1, H, W, sizes, inp.blend is not None)
+            rows.append({"sizes": sizes, "M": M, "us_per_frame": round(ms * 1e3, 2),
+                         "mpix_s": round(H * W / (ms / 1e3) / 1e6, 1), "kernel": kmd.last_kernel(),
+                         "roofline_frac": round(algo / (ms / 1e3) / 1e9 / peak, 3)})
+            del inp, out
+    if rank != 0:
+        return
+    full = rows[5]
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s vs fused sizes (sweep-M) and kernel size (sweep-k)", "value": full["mpix_s"],
+        "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": Wm, "ms_per_step": full["us_per_frame"] / 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{W}x{H}: M = 1..6 cumulative paper sizes, then M = 1 with k in 3..31 "
+                               "(SURVEY.md §8(d) sweep-M / sweep-k)"},
+        "sweep": rows, "clocks": clk.summary(), "gpu_launches": K * len(rows),
+        "paper_context": "reconstruction time grows with the number of fused kernels (PAPER.md:472, 654)"}),
+        flush=True)
+
+
+def run_batch(args, rank, world, local):
+    """BASELINE.json configs[4]: a batch of B 1080p frames per rank in ONE launch
+    (frame-parallel, no data-path collective; weak scaling over ranks)."""
+    from paper_2202_05977_b200 import inputs as gen
+    from paper_2202_05977_b200 import kmd
+    dev = torch.device("cuda", local)
+    H, W, B = args.height, args.width, args.batch
+    sizes = [int(x) for x in args.sizes.split(",")]
+    M = len(sizes)
+    # B distinct frames resident (frame ids rank*B ..): generated in chunks
+    rad = torch.empty((B, 3, H, W), device=dev)
+    imp = torch.empty((B, M, H, W), device=dev)
+    bl = torch.empty((B, M, H, W), device=dev) if M > 1 else None
+    for c0 in range(0, B, 16):
+        n = min(16, B - c0)
+        x = gen.make_inputs(n, H, W, M, frame_offset=rank * B + c0, device=dev)
+        rad[c0:c0 + n], imp[c0:c0 + n] = x.radiance, x.importance
+        if bl is not None:
+            bl[c0:c0 + n] = x.blend
+        del x
+    out = torch.empty((B, 3, H, W), device=dev)
+    K, Wm = max(3, args.steps // 400), max(3, args.warmup // 4)
+
+    def step(s):
+        kmd.decode_filter_fuse(rad, imp, bl, sizes, out=out)
+
+    for s in range(Wm):
+        step(s)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        a.record()
+        for s in range(K):
+            step(s)
+        b.record()
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    el = max_over_ranks(a.elapsed_time(b), world)
+    if rank != 0:
+        return
+    ms = el / K
+    algo = kmd.algorithmic_bytes(B, H, W, sizes, bl is not None)
+    peak = measured_peak_hbm()[0]
+    print(json.dumps({
+        "metric": f"{W}x{H} Mpix/s, batch of {B} frames per GPU in one launch", "value": B * H * W * world * K / (el / 1e3) / 1e6,
+        "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"batch {B} x {W}x{H}, sizes {sizes} (BASELINE.json configs[4])",
+                   "global_batch": B * world, "resident_gb": round((rad.numel() + imp.numel() + out.numel() + (bl.numel() if bl is not None else 0)) * 4 / 1e9, 1),
+                   "parallelism": f"frame-parallel x{world} (no data-path collective)"},
+        "ms_per_frame": ms / B,
+        "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": algo / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo,
+                     "kernel": kmd.last_kernel()},
+        "clocks": clk.summary(), "gpu_launches": K}), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup()
@@ -654,6 +778,10 @@ def main():
             run_bwd(args, rank, world, local)
         elif args.mode == "temporal":
             run_temporal(args, rank, world, local)
+        elif args.mode == "sweep":
+            run_sweep(args, rank, world, local)
+        elif args.mode == "batch":
+            run_batch(args, rank, world, local)
         else:
             run_kmd(args, rank, world, local)
     finally:

@@ -254,9 +254,9 @@ int32_t kmd_version(void);             /* KMD_VERSION_MAJOR*100 + KMD_VERSION_MI
 
 /* Diagnostic: which kernel the last fused launch on this host thread used
  * (0 none, 1 v1 direct (k > 13), 2 v2 warp-specialised (W % 4 != 0 or
- * unaligned), 3 v3 TMA with runtime M, 4 v3 TMA M = 6, 5 v3 TMA M = 6 with
- * the albedo epilogue, 6 v3 TMA M = 2).  Lets the tests prove which kernel
- * they exercised.                                                           */
+ * unaligned), 3 v3 TMA with runtime M, 100 + M v3 TMA compiled for that M,
+ * 150 + M the same with the albedo epilogue).  Lets the tests prove which
+ * kernel they exercised.                                                    */
 int32_t kmd_last_kernel(void);
 
 #ifdef __cplusplus

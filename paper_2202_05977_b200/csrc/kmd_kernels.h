@@ -41,7 +41,7 @@ cudaError_t launch_temporal(const float* cur_rad, const float* prev_rad, const f
                             int H, int W, float pos_tol, float normal_tol, float alpha, cudaStream_t st);
 
 // kernel variant of the last fused launch on this host thread (kmd_last_kernel)
-enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_TMA_M6 = 4, LK_TMA_M6_ALB = 5, LK_TMA_M2 = 6 };
+enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_TMA_SPEC = 100, LK_TMA_SPEC_ALB = 150 };
 void set_last_kernel(int k);
 
 }  // namespace kmd

@@ -676,19 +676,26 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
         kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
         return cudaGetLastError();
     };
-    // specialisations: the paper's M = 6 with softmax fusion, with
-    // and without the albedo epilogue, and the multi-resolution levels' M = 2
+    // specialisations: softmax fusion for M = 2..6 (the paper's M = 6, PAPER.md:324,
+    // the multi-resolution levels' M = 2, the sweep-M configurations), M = 6 with
+    // the albedo epilogue, and M = 1 (no fusion)
     const bool softmax = p.blend != nullptr && p.blend_is_logits, alb = p.albedo != nullptr;
-    if (!(p.debug & 2048) && softmax) {
-        if (p.M == 6) {
-            set_last_kernel(alb ? LK_TMA_M6_ALB : LK_TMA_M6);
-            return alb ? launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, true, 6>>)
-                       : launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6>>);
-        }
-        if (p.M == 2 && !alb) {
-            set_last_kernel(LK_TMA_M2);
-            return launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>);
-        }
+    if (!(p.debug & 2048)) {
+        auto spec = [&](auto kern, int code) {
+            set_last_kernel(code);
+            return launch(kern);
+        };
+        if (softmax && !alb) switch (p.M) {
+                case 2: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>, LK_TMA_SPEC + 2);
+                case 3: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 3>>, LK_TMA_SPEC + 3);
+                case 4: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 4>>, LK_TMA_SPEC + 4);
+                case 5: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 5>>, LK_TMA_SPEC + 5);
+                case 6: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6>>, LK_TMA_SPEC + 6);
+                default: break;
+            }
+        if (softmax && alb && p.M == 6)
+            return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, true, 6>>, LK_TMA_SPEC_ALB + 6);
+        if (p.M == 1 && !alb) return spec(fused_tma_kernel<Spec<FUSE_ONE, false, 1>>, LK_TMA_SPEC + 1);
     }
     set_last_kernel(LK_TMA);
     return launch(fused_tma_kernel<Runtime>);

@@ -310,13 +310,18 @@ def launches_per_call() -> int:
     return int(lib().kmd_launches_per_call())
 
 
-LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma", 4: "v3-tma-M6", 5: "v3-tma-M6-albedo",
-               6: "v3-tma-M2"}
+LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma"}
 
 
 def last_kernel() -> str:
-    """Kernel variant of the last fused launch on this thread (diagnostic)."""
-    return LAST_KERNEL.get(int(lib().kmd_last_kernel()), "?")
+    """Kernel variant of the last fused launch on this thread (diagnostic):
+    v1-direct, v2-ws, v3-tma (runtime M), v3-tma-M<m>[-albedo] (compiled for M)."""
+    code = int(lib().kmd_last_kernel())
+    if code >= 150:
+        return f"v3-tma-M{code - 150}-albedo"
+    if code >= 100:
+        return f"v3-tma-M{code - 100}"
+    return LAST_KERNEL.get(code, "?")
 
 
 def version() -> int:

@@ -69,12 +69,13 @@ def test_shapes_fuzz(oracle_mod, cuda_device, N, H, W, sizes):
     (1, 28, 56, [13]),                      # M = 1, the largest TMA window
     (3, 54, 104, [13, 3, 9, 5, 11, 7]),     # M = 6 specialisation, unsorted sizes, N = 3
     (1, 13, 16, [13, 13]),                  # H == k: every row is a border row
+    (1, 57, 112, [3, 5, 7, 9, 11, 13, 3, 5]),  # M = 8: the runtime-M kernel
 ])
 def test_tma_kernel_shapes(oracle_mod, cuda_device, N, H, W, sizes):
     """W % 4 == 0: the TMA kernel (kmd_tma.cu) and its specialisations."""
     inp = gen.make_inputs(N, H, W, len(sizes), seed=2000 + H * W)
     out = _run(inp, sizes, cuda_device)
-    expect = {6: "v3-tma-M6", 2: "v3-tma-M2"}.get(len(sizes), "v3-tma")
+    expect = f"v3-tma-M{len(sizes)}" if len(sizes) <= 6 else "v3-tma"
     assert kmd.last_kernel() == expect
     assert_parity(out, _oracle(oracle_mod, inp, sizes), what=f"tma {N}x{H}x{W} {sizes}")
 
