@@ -112,6 +112,18 @@ def test_1080p_sampled_in_bench_configuration(oracle_mod, cuda_device):
     assert_parity(gpu[0][:, ys, xs].T, ref, what="1080p random pixels")
 
 
+def test_4k_frame_sampled(oracle_mod, cuda_device):
+    # configs[3]'s frame on one GPU: rows at the top / middle / bottom tile rows
+    # (2160 = 80 tile rows of 27) and the right-most partial tile column
+    H, W = 2160, 3840
+    inp = gen.make_inputs(1, H, W, 6, seed=4)
+    gpu = _run(inp, PAPER, cuda_device)
+    assert kmd.last_kernel() == "v3-tma-M6"
+    for y0, y1 in [(0, 30), (1077, 1090), (2140, 2160)]:
+        ref = _oracle(oracle_mod, inp, PAPER, rows=(y0, y1))
+        assert_parity(gpu[:, :, y0:y1], ref, what=f"4K rows {y0}:{y1}")
+
+
 def test_batch_of_1080p_frames_sampled(oracle_mod, cuda_device):
     # configs[4] shape (a batch of 1080p frames in one launch), 3 frames sampled
     N, H, W = 4, 1080, 1920
