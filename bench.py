@@ -577,7 +577,10 @@ def run_bwd(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / peak,
                      "algorithmic_bytes_per_launch": algo,
-                     "note": f"{kmd.backward_launches_per_call(M)} launches per step; algorithmic = inputs + outputs once"},
+                     "kernel": kmd.last_kernel(),
+                     "note": f"{kmd.backward_launches_per_call(M)} launches per step (pass A: h_i and G.R_i, pass B: "
+                             "transposed box + dL/dI, pass C: dL/dB); algorithmic = inputs + outputs once, the "
+                             "h_i workspace (16 M B/px written and read) is not counted"},
         "clocks": clk.summary(), "gpu_launches": steps * kmd.backward_launches_per_call(M)}),
         flush=True)
 

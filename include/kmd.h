@@ -201,11 +201,12 @@ kmd_status kmd_combine_resolutions(const float* fine, const float* coarse, const
  * SPEC.md:289-297).  Given grad_out = dL/dRhat [N,3,H,W] (device):
  *   grad_importance [N,M,H,W] = dL/dI_i,  grad_blend [N,M,H,W] = dL/dB_i
  *   (dL/dalpha_i when blend_is_logits == 0; may be NULL; zeros when M == 1).
- * The radiance gradient is not computed (rendered data).  The
- * forward box sums are recomputed per 32 x 64 tile in shared memory (one
- * launch); importance must lie in (-80, 80) (unshifted exp).  The workspace
- * is kmd_backward_workspace_bytes(...) bytes of device memory (currently 0:
- * workspace may be NULL).                                                   */
+ * The radiance gradient is not computed (rendered data).
+ * Importance must lie in (-80, 80) (unshifted exp).  With a device workspace
+ * of kmd_backward_workspace_bytes(...) bytes (16 M B per pixel: the per-size
+ * gradient field h_i), W % 4 == 0, k <= 13 and 16-byte aligned buffers the
+ * TMA passes run (kmd_last_kernel() == 11); otherwise (or with workspace ==
+ * NULL) a one-launch tiled kernel that needs no workspace (== 10).          */
 size_t kmd_backward_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg);
 kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* importance,
                                            const float* blend, const float* grad_out,

@@ -529,7 +529,8 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
 // NEXT row 3: backward
 size_t kmd_backward_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg) {
     if (!cfg || N < 1 || H < 1 || W < 1 || cfg->num_sizes < 1 || cfg->num_sizes > KMD_MAX_SIZES) return 0;
-    return kmd::bwd_workspace_floats(H, W, cfg->num_sizes) * sizeof(float);
+    // the h_i field of the TMA path (pass A -> pass B); the one-launch fallback needs none
+    return kmd::bwd_tma_workspace_bytes(N, H, W, cfg->num_sizes);
 }
 
 kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* importance, const float* blend,
@@ -549,9 +550,20 @@ kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* i
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
     if (workspace_bytes < kmd_backward_workspace_bytes(N, H, W, cfg))
         return fail(KMD_ERR_DIM, "workspace too small");
-    cudaError_t e = kmd::launch_backward(radiance, importance, cfg->num_sizes > 1 ? blend : nullptr, grad_out,
-                                         grad_importance, grad_blend, N, H, W, cfg->num_sizes, cfg->sizes,
-                                         cfg->blend_is_logits, (float*)workspace, (cudaStream_t)stream);
+    const int M = cfg->num_sizes;
+    cudaError_t e;
+    if (workspace && kmd::bwd_tma_supported(H, W, M, cfg->sizes, radiance, importance, grad_out, workspace) &&
+        (M == 1 || ((uintptr_t)blend & 15) == 0)) {
+        kmd::set_last_kernel(kmd::LK_BWD_TMA);
+        e = kmd::launch_backward_tma(radiance, importance, M > 1 ? blend : nullptr, grad_out, grad_importance,
+                                     grad_blend, N, H, W, M, cfg->sizes, cfg->blend_is_logits, workspace,
+                                     (cudaStream_t)stream);
+    } else {
+        kmd::set_last_kernel(kmd::LK_BWD_TILE);
+        e = kmd::launch_backward(radiance, importance, M > 1 ? blend : nullptr, grad_out, grad_importance,
+                                 grad_blend, N, H, W, M, cfg->sizes, cfg->blend_is_logits, (float*)workspace,
+                                 (cudaStream_t)stream);
+    }
     return e == cudaSuccess ? KMD_OK : cuda_fail(e, "backward launch");
 }
 

@@ -1,0 +1,432 @@
+// kmd_bwd_tma.cu -- NEXT row 3, fast path: the backward of the fused decoder
+// as three TMA / elementwise passes (Eq. 1: the kernel
+// maps are trained end to end through Eq. 3-5).
+//
+//   pass A (kmd_tma.cu, SpecBwdH): the forward's tiles and box sums; per size i
+//          and pixel p the fusion warps write h_i(p) = (a_i G / den_i,
+//          a_i G.R_i / den_i) (a_i = softmax_i(B)(p), G = dL/dRhat(p)) to a
+//          workspace, and G.R_i(p) to grad_blend;
+//   pass B (here): T_i = Bt(h_i), the transposed clamp-to-edge box: the same
+//          warp-specialised pipeline with the field = h_i (zero outside the
+//          frame: TMA's out-of-bounds fill) and the clamped taps folded back
+//          onto the border rows (field warps) and columns (fusion warps); the
+//          fusion warps finish dL/dI_i(q) = e_i(q) (r(q) . T_i.xyz - T_i.w);
+//   pass C (here): dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), elementwise.
+//
+// Pass B per CTA (one per SM), per 52 x 27 tile, per size i:
+//   warp 0       TMA: the h_i box [39][68] float4 as two 34-column halves
+//                (2-deep ring) and the I_i
+//                box [27][56] of the tile's own pixels (4-deep ring);
+//   warps 1-4    field: vertical Gil-Werman sums of h_i per column (+ folds);
+//   warps 5-11   fusion: horizontal sums (+ folds), the dL/dI epilogue.
+// Unshifted exp: importance in (-80, 80) (header note).
+#include <cuda.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "kmd_common.cuh"
+#include "kmd_gw.cuh"
+#include "kmd_kernels.h"
+
+namespace kmd {
+namespace bwd {
+
+constexpr int RMAX = 6;
+constexpr int TW = 52, TH = 27, FH = TH + 2 * RMAX;  // 39 field rows
+constexpr int XOFF = 8, BW = 68, VS = 68, BBW = 56;
+constexpr int SEG = 7, NSEG = 8;
+constexpr int NH = 2, NB = 4, NV = 3;
+constexpr int NFIELD = 4, NFUSE = (TH * NSEG + 31) / 32;  // 7
+constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
+constexpr float L2E = 1.44269502162933349609375f;
+constexpr float LN2_HI = 0.693147182464599609375f;
+
+// h_i box: rows y0-6 .. y0+32, columns x0-8 .. x0+59 (zero outside the frame),
+// loaded as two 34-column halves (TMA boxes of 136 floats: a float4 innermost
+// dimension would make TMA move 16-byte rows); field half h reads half h only
+constexpr int HBW = 34;
+struct alignas(128) HHalf {            // 128-byte aligned: a TMA destination
+    float4 h[FH][HBW];
+};
+struct HSlot {
+    HHalf half[2];
+};
+struct alignas(128) Slot {
+    float4 V[TH][VS];                  // Bt_y(h_i) by field column
+};
+struct alignas(128) ISlot {
+    float I[TH][BBW];                  // I_i at the tile's pixels
+};
+static_assert(sizeof(HHalf) % 128 == 0, "TMA destinations 128-B aligned");
+struct Smem {
+    HSlot hs[NH];
+    Slot slot[NV];
+    ISlot is[NB];
+    unsigned long long h_full[NH], h_empty[NH], v_full[NV], v_empty[NV], i_full[NB], i_empty[NB];
+};
+
+struct BParams {
+    const float* rad;    // [N,3,H,W]
+    const float* imp;    // [N,M,H,W]
+    float* gI;           // [N,M,H,W]
+    int N, H, W, M;
+    unsigned rpack;      // radius of size i in bits 4i..4i+3
+    int debug;           // development switches (env KMD_DEBUG): 1 = no gI stores
+};
+
+__device__ __forceinline__ float exp_acc(float x) {  // as kmd_tma.cu
+    const float t = x * L2E;
+    const float r = fmaf(-t, LN2_HI, x);
+    const float e = ex2_approx(t);
+    return fmaf(e, r, e);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float4 fma4(float m, float4 a, float4 v) {
+    return make_float4(fmaf(m, a.x, v.x), fmaf(m, a.y, v.y), fmaf(m, a.z, v.z), fmaf(m, a.w, v.w));
+}
+
+// field: vertical transposed box of h over a column, N = TH outputs, plus the
+// folds of the clamped taps at the frame's first / last row (1-D multiplicity
+// of source s at q = 0 is R - s + 1, i.e. R - s extra; mirrored at q = H - 1)
+template <int R>
+__device__ __forceinline__ void field_job(const HSlot& hs, Slot& sl, int c, int half, int cc, int y0, int H) {
+    const float4(&hh)[FH][HBW] = hs.half[half].h;
+    const float4* hb = &hh[RMAX - R][cc];
+    float4* Vc = &sl.V[0][c];
+    gw_line_field<R, TH>([&](int f) { return hb[f * HBW]; }, [&](int oy, float4 v) { Vc[oy * VS] = v; });
+    // folds of the clamped taps, only in the frame's first / last tile row (kept
+    // out of the Gil-Werman emits: inlining them there bloated the hot code)
+    if (y0 == 0) {
+        float4 v = Vc[0];
+        for (int s = 0; s < R && s < H; ++s) v = fma4((float)(R - s), hh[RMAX + s][cc], v);
+        Vc[0] = v;
+    }
+    if (H - 1 - y0 < TH) {
+        const int oy = H - 1 - y0;
+        float4 v = Vc[oy * VS];
+        for (int s = max(H - R, 0); s < H; ++s) v = fma4((float)(s + R - H + 1), hh[RMAX + s - y0][cc], v);
+        Vc[oy * VS] = v;
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)[SEG]) {
+    const float4* Vr = &sl.V[ty][xs + RMAX - R];
+    gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    bwd_t_kernel(const __grid_constant__ BParams p, const __grid_constant__ CUtensorMap tm_h,
+                 const __grid_constant__ CUtensorMap tm_i, int tiles_x, int tiles_y, int n_tiles) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int M = p.M;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NH; ++s) {
+            mbar_init(&sm.h_full[s], 1);
+            mbar_init(&sm.h_empty[s], 2);
+        }
+        for (int s = 0; s < NV; ++s) {
+            mbar_init(&sm.v_full[s], 2);
+            mbar_init(&sm.v_empty[s], NFUSE);
+        }
+        for (int s = 0; s < NB; ++s) {
+            mbar_init(&sm.i_full[s], 1);
+            mbar_init(&sm.i_empty[s], NFUSE);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int per_frame = tiles_x * tiles_y;
+    auto tile = [&](int tl, int& n, int& x0, int& y0) {
+        const int t = blockIdx.x + tl * gridDim.x;
+        n = t / per_frame;
+        const int r = t - n * per_frame, ty = r / tiles_x;
+        x0 = (r - ty * tiles_x) * TW;
+        y0 = ty * TH;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int tl = 0; tl < my_tiles; ++tl) {
+                int n, x0, y0;
+                tile(tl, n, x0, y0);
+                for (int i = 0; i < M; ++i) {
+                    const int seq = tl * M + i, sh = seq % NH, sb = seq % NB;
+                    mbar_wait(&sm.h_empty[sh], ((seq / NH) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.h_full[sh], 2 * FH * HBW * 16);
+                    tma_load_3d(&sm.hs[sh].half[0].h[0][0], &tm_h, 4 * (x0 - XOFF), y0 - RMAX, n * M + i,
+                                &sm.h_full[sh]);
+                    tma_load_3d(&sm.hs[sh].half[1].h[0][0], &tm_h, 4 * (x0 - XOFF + HBW), y0 - RMAX, n * M + i,
+                                &sm.h_full[sh]);
+                    mbar_wait(&sm.i_empty[sb], ((seq / NB) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.i_full[sb], TH * BBW * 4);
+                    tma_load_3d(&sm.is[sb].I[0][0], &tm_i, x0, y0, n * M + i, &sm.i_full[sb]);
+                }
+            }
+        }
+    } else if (warp <= NFIELD) {
+        const int fw = warp - 1;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+            int n, x0, y0;
+            tile(tl, n, x0, y0);
+            (void)n;
+#pragma unroll 1
+            for (int jl = fw; jl < 2 * M; jl += NFIELD) {
+                const int i = jl >> 1, h = jl & 1;
+                const int seq = tl * M + i, sh = seq % NH, sv = seq % NV;
+                // field column c <-> global x0 - 6 + c <-> column c + 2 - 34 h of half h
+                // (unclamped: zero outside the frame)
+                const int c = h * 32 + lane, cc = c + XOFF - RMAX - HBW * h;
+                mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);
+                mbar_wait(&sm.h_full[sh], (seq / NH) & 1);
+                switch ((p.rpack >> (4 * i)) & 15) {
+                    case 0: field_job<0>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 1: field_job<1>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 2: field_job<2>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 3: field_job<3>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 4: field_job<4>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 5: field_job<5>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    default: field_job<6>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.h_empty[sh]);
+                    mbar_arrive(&sm.v_full[sv]);
+                }
+            }
+        }
+    } else {
+        const int c = threadIdx.x - (1 + NFIELD) * 32;
+        const int ty = c / NSEG, sub = c % NSEG;
+        const bool active = ty < TH;
+        const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
+        const int len = (0x76677766u >> (4 * sub)) & 0xf;
+        const size_t plane = (size_t)p.H * p.W;
+        int vs = 0, vph = 0, bs = 0, bph = 0;
+        for (int tl = 0; tl < my_tiles; ++tl) {
+            int n, x0, y0;
+            tile(tl, n, x0, y0);
+            const int gy = y0 + ty, gyc = min(gy, p.H - 1);
+            const bool row_ok = active && gy < p.H;
+            const bool edge_x = x0 == 0 || x0 + TW >= p.W;
+            float rr[SEG][3];
+            const float* rp = p.rad + (size_t)n * 3 * plane + (size_t)gyc * p.W;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const int gx = min(x0 + xs + j, p.W - 1);
+                rr[j][0] = __ldg(rp + gx);
+                rr[j][1] = __ldg(rp + plane + gx);
+                rr[j][2] = __ldg(rp + 2 * plane + gx);
+            }
+#pragma unroll 1
+            for (int i = 0; i < M; ++i) {
+                mbar_wait(&sm.v_full[vs], vph);
+                mbar_wait(&sm.i_full[bs], bph);
+                if (active) {
+                    const int R = (p.rpack >> (4 * i)) & 15;
+                    const Slot& sl = sm.slot[vs];
+                    float4 o[SEG];
+                    switch (R) {
+                        case 0: hbox<0>(sl, ty, xs, o); break;
+                        case 1: hbox<1>(sl, ty, xs, o); break;
+                        case 2: hbox<2>(sl, ty, xs, o); break;
+                        case 3: hbox<3>(sl, ty, xs, o); break;
+                        case 4: hbox<4>(sl, ty, xs, o); break;
+                        case 5: hbox<5>(sl, ty, xs, o); break;
+                        default: hbox<6>(sl, ty, xs, o); break;
+                    }
+                    const float* Ir = &sm.is[bs].I[ty][xs];
+                    float* go = p.gI + ((size_t)n * M + i) * plane + (size_t)gyc * p.W;
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) {
+                        const int gx = x0 + xs + j;
+                        if (j < len && row_ok && gx < p.W && !(p.debug & 1)) {
+                            float4 v = o[j];
+                            if (edge_x) {  // horizontal folds at the frame's first / last column
+                                if (gx == 0)
+                                    for (int s = 0; s < R && s < p.W; ++s)
+                                        v = fma4((float)(R - s), sl.V[ty][s - x0 + RMAX], v);
+                                if (gx == p.W - 1)
+                                    for (int s = max(p.W - R, 0); s < p.W; ++s)
+                                        v = fma4((float)(s + R - p.W + 1), sl.V[ty][s - x0 + RMAX], v);
+                            }
+                            const float e = exp_acc(Ir[j]);
+                            go[gx] = e * (fmaf(rr[j][0], v.x, fmaf(rr[j][1], v.y, rr[j][2] * v.z)) - v.w);
+                        }
+                    }
+                }
+                __syncwarp();
+                if ((c & 31) == 0) {
+                    mbar_arrive(&sm.v_empty[vs]);
+                    mbar_arrive(&sm.i_empty[bs]);
+                }
+                if (++vs == NV) { vs = 0; vph ^= 1; }
+                if (++bs == NB) { bs = 0; bph ^= 1; }
+            }
+        }
+    }
+}
+
+// pass C: dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), a = softmax(B) (logits)
+__global__ void __launch_bounds__(256) bwd_blend_kernel(const float* __restrict__ blend, float* __restrict__ gB,
+                                                        int N, int M, long long plane) {
+    const long long total = (long long)N * plane;
+    for (long long t = blockIdx.x * 256LL + threadIdx.x; t < total; t += (long long)gridDim.x * 256) {
+        const long long n = t / plane, q = t - n * plane;
+        const float* b = blend + n * M * plane + q;
+        float* g = gB + n * M * plane + q;
+        float bv[KMD_MAX_SIZES], d[KMD_MAX_SIZES];
+        float m = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i)
+            if (i < M) {
+                bv[i] = __ldg(b + i * plane);
+                d[i] = g[i * plane];
+                m = fmaxf(m, bv[i]);
+            }
+        float s = 0.f, mean = 0.f;
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i)
+            if (i < M) {
+                bv[i] = expf(bv[i] - m);
+                s += bv[i];
+                mean = fmaf(bv[i], d[i], mean);
+            }
+        const float inv = 1.f / s;
+        mean *= inv;
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i)
+            if (i < M) g[i * plane] = bv[i] * inv * (d[i] - mean);
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    });
+    return fn;
+}
+
+bool encode(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+            const cuuint32_t* box) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace bwd
+
+bool bwd_tma_supported(int H, int W, int M, const int* sizes, const void* a, const void* b, const void* c,
+                       const void* d) {
+    if (M < 1 || M > KMD_MAX_SIZES || W % 4 != 0) return false;
+    for (int i = 0; i < M; ++i)
+        if ((sizes[i] - 1) / 2 > bwd::RMAX) return false;
+    if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)d) & 15) return false;
+    (void)H;
+    return bwd::get_encode() != nullptr;
+}
+
+size_t bwd_tma_workspace_bytes(int N, int H, int W, int M) { return (size_t)N * M * H * W * sizeof(float4); }
+
+cudaError_t launch_backward_tma(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
+                                float* gB, int N, int H, int W, int M, const int* sizes, int logits, void* ws,
+                                cudaStream_t st) {
+    using namespace bwd;
+    float4* hbuf = reinterpret_cast<float4*>(ws);
+    // ---- pass A: h_i and G.R_i (the forward kernel's tiles and box sums)
+    FusedParams p{};
+    p.rad = rad;
+    p.imp = imp;
+    p.blend = M > 1 ? blend : nullptr;
+    p.N = N;
+    p.W = W;
+    p.H = H;
+    p.row_base = 0;
+    p.buf_rows = H;
+    p.out_y0 = 0;
+    p.out_rows = H;
+    p.M = M;
+    p.blend_is_logits = logits;
+    unsigned rpack = 0;
+    int rmax = 0;
+    for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < M ? sizes[i] : 1;
+    for (int i = 0; i < M; ++i) {
+        const int r = (sizes[i] - 1) / 2;
+        rmax = r > rmax ? r : rmax;
+        rpack |= (unsigned)r << (4 * i);
+    }
+    p.rmax = rmax;
+    p.grad = G;
+    p.hbuf = hbuf;
+    p.dotbuf = M > 1 ? gB : nullptr;
+    static const int dbg = [] { const char* s = getenv("KMD_DEBUG"); return s ? atoi(s) : 0; }();
+    p.debug = dbg;
+    cudaError_t e = launch_bwd_h_tma(p, st);
+    if (e != cudaSuccess) return e;
+    // ---- pass B: transposed box of h_i, dL/dI_i
+    BParams q{rad, imp, gI, N, H, W, M, rpack, dbg};
+    CUtensorMap m_h, m_i;
+    {
+        // h as a 3-D [N*M][H][4W] float array; boxes of 34 float4 = 136 floats
+        const cuuint64_t dims[3] = {4 * (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N * M};
+        const cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)W * H * 16};
+        const cuuint32_t box[3] = {4 * HBW, FH, 1};
+        if (!encode(&m_h, 3, hbuf, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N * M};
+        const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+        const cuuint32_t box[3] = {BBW, TH, 1};
+        if (!encode(&m_i, 3, imp, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    const int tiles_y = (H + TH - 1) / TH, tiles_x = (W + TW - 1) / TW;
+    const long long n_tiles = (long long)tiles_x * tiles_y * N;
+    if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
+    int dev = 0, sms = 148;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    const size_t smem = sizeof(Smem);
+    if ((e = cudaFuncSetAttribute(bwd_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+        return e;
+    const int grid = (int)(n_tiles < sms ? n_tiles : sms);
+    bwd_t_kernel<<<grid, NTHREADS, smem, st>>>(q, m_h, m_i, tiles_x, tiles_y, (int)n_tiles);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // ---- pass C: dL/dB
+    if (gB && M == 1) return cudaMemsetAsync(gB, 0, sizeof(float) * (size_t)N * H * W, st);
+    if (gB && logits) {
+        const long long total = (long long)N * H * W;
+        const long long need = (total + 255) / 256;
+        const int g = (int)(need < (long long)sms * 16 ? need : (long long)sms * 16);
+        bwd_blend_kernel<<<g, 256, 0, st>>>(blend, gB, N, M, (long long)H * W);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;  // alpha given: dL/dalpha_i = G.R_i, written by pass A
+}
+
+}  // namespace kmd

@@ -28,7 +28,15 @@ cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, 
 cudaError_t launch_combine(const float* fine, const float* coarse, const float* alpha, float* out, int N, int H,
                            int W, cudaStream_t st);
 
-// backward (NEXT row 3; kmd_bwd.cu)
+// backward (NEXT row 3): pass A in kmd_tma.cu (h_i, G.R_i), pass B / C in
+// kmd_bwd_tma.cu, the one-launch fallback in kmd_bwd.cu
+cudaError_t launch_bwd_h_tma(FusedParams p, cudaStream_t stream);
+bool bwd_tma_supported(int H, int W, int M, const int* sizes, const void* a, const void* b, const void* c,
+                       const void* d);
+size_t bwd_tma_workspace_bytes(int N, int H, int W, int M);
+cudaError_t launch_backward_tma(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
+                                float* gB, int N, int H, int W, int M, const int* sizes, int logits, void* ws,
+                                cudaStream_t st);
 size_t bwd_workspace_floats(int H, int W, int M);
 cudaError_t launch_backward(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
                             float* gB, int N, int H, int W, int M, const int* sizes, int logits, float* ws,
@@ -41,7 +49,8 @@ cudaError_t launch_temporal(const float* cur_rad, const float* prev_rad, const f
                             int H, int W, float pos_tol, float normal_tol, float alpha, cudaStream_t st);
 
 // kernel variant of the last fused launch on this host thread (kmd_last_kernel)
-enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_TMA_SPEC = 100, LK_TMA_SPEC_ALB = 150 };
+enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_BWD_TILE = 10, LK_BWD_TMA = 11, LK_TMA_SPEC = 100,
+                  LK_TMA_SPEC_ALB = 150 };
 void set_last_kernel(int k);
 
 }  // namespace kmd

@@ -217,7 +217,7 @@ struct Acc {
 // reading R2), acc += a_i R_i, S += a_i, and Rhat = acc / S at the end.  A
 // logit beyond the fp32 exp range (S = 0 or inf, non-finite acc) or a tiny box
 // denominator sends the pixel to the exact path (reading R13).
-enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2 };
+enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2, FUSE_BWD_H = 3 };
 
 template <int MODE>
 __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alpha */, float4 v) {
@@ -335,6 +335,13 @@ struct Runtime {
     static constexpr int M = 0;
     static constexpr int MODE = -1;
     static constexpr bool ALB = true;
+};
+// backward pass A (NEXT row 3): the forward's tiles and box sums, with the
+// fusion epilogue replaced by the per-size gradient field h_i (runtime M)
+struct SpecBwdH {
+    static constexpr int M = 0;
+    static constexpr int MODE = FUSE_BWD_H;
+    static constexpr bool ALB = false;
 };
 template <int MODE_, bool ALB_, int M_>
 struct Spec {
@@ -497,6 +504,87 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int vs = 0, vph = 0, bs = 0, bph = 0;  // V / blend ring slot and phase of the current step
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            if constexpr (SP::MODE == FUSE_BWD_H) {
+                // ---- backward pass A: h_i and G.R_i at this thread's pixels --------
+                // (whole frame: row_base = out_y0 = 0, buf_rows = out_rows = H)
+                const int gy = tc.y0 + ty;
+                const bool row_ok = active && gy < p.H;
+                const size_t plane = (size_t)p.H * p.W;
+                const int gyc = min(gy, p.H - 1);
+                const float* gp = p.grad + (size_t)tc.n * 3 * plane + (size_t)gyc * p.W;
+                const float* bp = p.blend ? p.blend + (size_t)tc.n * M * plane + (size_t)gyc * p.W : nullptr;
+                const bool logits = M > 1 && p.blend_is_logits;
+                float G[SEG][3], mb[SEG], is[SEG];
+#pragma unroll
+                for (int j = 0; j < SEG; ++j) {
+                    const int gx = min(tc.x0 + xs + j, p.W - 1);
+                    G[j][0] = __ldg(gp + gx);
+                    G[j][1] = __ldg(gp + plane + gx);
+                    G[j][2] = __ldg(gp + 2 * plane + gx);
+                    mb[j] = 0.f;
+                    is[j] = 1.f;
+                }
+                if (logits) {
+                    // softmax shift and normaliser of the logits (Eq. 5): every load
+                    // issued before any is used (a dependent chain per pixel would
+                    // expose one L2 latency per logit)
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) {
+                        const int gx = min(tc.x0 + xs + j, p.W - 1);
+                        float b[KMD_MAX_SIZES];
+#pragma unroll
+                        for (int i = 0; i < KMD_MAX_SIZES; ++i) b[i] = i < M ? __ldg(bp + i * plane + gx) : -INFINITY;
+                        float m = b[0];
+#pragma unroll
+                        for (int i = 1; i < KMD_MAX_SIZES; ++i) m = fmaxf(m, b[i]);
+                        float sum = 0.f;
+#pragma unroll
+                        for (int i = 0; i < KMD_MAX_SIZES; ++i) sum += i < M ? exp_acc(b[i] - m) : 0.f;
+                        mb[j] = m;
+                        is[j] = rcp_approx(sum);
+                    }
+                }
+#pragma unroll 1
+                for (int i = 0; i < M; ++i) {
+                    IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
+                    if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
+                    if (active && !(p.debug & 64)) {
+                        float4 o[SEG];
+                        switch ((rpack >> (4 * i)) & 15) {
+                            case 0: hbox<0>(sm.slot[vs], ty, xs, o); break;
+                            case 1: hbox<1>(sm.slot[vs], ty, xs, o); break;
+                            case 2: hbox<2>(sm.slot[vs], ty, xs, o); break;
+                            case 3: hbox<3>(sm.slot[vs], ty, xs, o); break;
+                            case 4: hbox<4>(sm.slot[vs], ty, xs, o); break;
+                            case 5: hbox<5>(sm.slot[vs], ty, xs, o); break;
+                            default: hbox<6>(sm.slot[vs], ty, xs, o); break;
+                        }
+                        const float* Br = &sm.bl[bs].B[ty][xs];
+                        const size_t base = ((size_t)tc.n * M + i) * plane + (size_t)gyc * p.W;
+#pragma unroll
+                        for (int j = 0; j < SEG; ++j) {
+                            const int gx = tc.x0 + xs + j;
+                            if (j < len && row_ok && gx < p.W && !(p.debug & 1)) {
+                                const float rden = rcp_approx(o[j].x);
+                                const float R0 = o[j].y * rden, R1 = o[j].z * rden, R2 = o[j].w * rden;
+                                const float a = M == 1 ? 1.f : (logits ? exp_acc(Br[j] - mb[j]) * is[j] : Br[j]);
+                                const float dot = fmaf(G[j][0], R0, fmaf(G[j][1], R1, G[j][2] * R2));
+                                const float ar = a * rden;
+                                p.hbuf[base + gx] = make_float4(ar * G[j][0], ar * G[j][1], ar * G[j][2], ar * dot);
+                                if (p.dotbuf) p.dotbuf[base + gx] = dot;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if ((c & 31) == 0) {
+                        mbar_arrive(&sm.v_empty[vs]);
+                        if (has_blend) mbar_arrive(&sm.b_empty[bs]);
+                    }
+                    if (++vs == NV) { vs = 0; vph ^= 1; }
+                    if (++bs == NB) { bs = 0; bph ^= 1; }
+                }
+                continue;
+            }
             // albedo of this thread's pixels, loaded now so the latency hides
             // behind the M sizes (remodulation epilogue)
             float alb[SEG][3];
@@ -637,6 +725,36 @@ extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, tma::g_instr, sizeof(unsigned long long) * n);
 }
 #endif
+
+// backward pass A (NEXT row 3, kmd_bwd_tma.cu): whole frames only
+cudaError_t launch_bwd_h_tma(FusedParams p, cudaStream_t stream) {
+    using namespace tma;
+    p.tile_y_begin = 0;
+    const int tiles_y = (p.H + TH - 1) / TH, tiles_x = (p.W + TW - 1) / TW;
+    const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
+    if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
+    CUtensorMap m_rad, m_imp, m_blend, m_out;
+    if (!make_map(&m_rad, p.rad, p.W, p.H, 3LL * p.N, BW, FH, 3) ||
+        !make_map(&m_imp, p.imp, p.W, p.H, (long long)p.M * p.N, BW, FH, 1))
+        return cudaErrorInvalidValue;
+    if (p.blend) {
+        if (!make_map(&m_blend, p.blend, p.W, p.H, (long long)p.M * p.N, BBW, TH, 1)) return cudaErrorInvalidValue;
+    } else {
+        m_blend = m_imp;
+    }
+    m_out = m_rad;  // no store
+    int dev = 0, sms = 148;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    const size_t smem = sizeof(Smem);
+    auto kern = fused_tma_kernel<SpecBwdH>;
+    if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return err;
+    const int grid = (int)(n_tiles < sms ? n_tiles : sms);
+    kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
+    return cudaGetLastError();
+}
 
 bool tma_supported(const FusedParams& p) {
     if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % 4 != 0) return false;

@@ -310,7 +310,7 @@ def launches_per_call() -> int:
     return int(lib().kmd_launches_per_call())
 
 
-LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma"}
+LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma", 10: "bwd-tile", 11: "bwd-tma"}
 
 
 def last_kernel() -> str:
@@ -434,9 +434,13 @@ def decode_filter_fuse_backward(radiance: torch.Tensor, importance: torch.Tensor
     return grad_importance, grad_blend
 
 
-def backward_launches_per_call(M: int) -> int:
-    """Kernel launches of one decode_filter_fuse_backward call (one tiled kernel;
-    plus a memset of grad_blend when M == 1)."""
+def backward_launches_per_call(M: int, path: Optional[str] = None) -> int:
+    """Kernel launches of one decode_filter_fuse_backward call: the TMA path
+    ("bwd-tma") runs pass A, pass B and pass C (or a memset when M == 1); the
+    one-launch tiled fallback ("bwd-tile") adds a memset when M == 1."""
+    path = path or last_kernel()
+    if path == "bwd-tma":
+        return 3
     return 1 if M > 1 else 2
 
 

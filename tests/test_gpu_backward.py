@@ -37,7 +37,10 @@ def _normwise(gpu, ref, what):
 
 
 @pytest.mark.parametrize("N,H,W,sizes,logits", [
-    (1, 96, 160, PAPER, True),
+    (1, 96, 160, PAPER, True),              # TMA passes (W % 4 == 0)
+    (2, 61, 108, [3, 5, 7], True),          # TMA, ragged 52x27 tiles, N = 2
+    (1, 28, 56, [13], True),                # TMA, M = 1
+    (1, 55, 104, [5, 3, 11], False),        # TMA, alpha given
     (2, 37, 53, [3, 5, 7], True),
     (1, 40, 44, [3, 9], False),
     (1, 33, 70, [5], True),
@@ -56,6 +59,7 @@ def test_backward_matches_oracle(oracle_mod, cuda_device, N, H, W, sizes, logits
                                              None if blend is None else blend.to(dev), G.to(dev),
                                              sizes, blend_is_logits=logits)
     torch.cuda.synchronize()
+    assert kmd.last_kernel() == ("bwd-tma" if W % 4 == 0 else "bwd-tile")
     rI, rB = oracle_mod.backward(inp.radiance.numpy(), inp.importance.numpy(),
                                  None if blend is None else blend.numpy(), G.numpy().astype(np.float64),
                                  sizes, blend_is_logits=logits)
