@@ -280,36 +280,64 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-// pass C: dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), a = softmax(B) (logits)
+// pass C: dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), a = softmax(B) (logits).
+// One thread per 4 consecutive pixels of a frame (float4 when plane % 4 == 0);
+// blockIdx.y = frame, so no 64-bit division per element.
+template <bool VEC>
 __global__ void __launch_bounds__(256) bwd_blend_kernel(const float* __restrict__ blend, float* __restrict__ gB,
-                                                        int N, int M, long long plane) {
-    const long long total = (long long)N * plane;
-    for (long long t = blockIdx.x * 256LL + threadIdx.x; t < total; t += (long long)gridDim.x * 256) {
-        const long long n = t / plane, q = t - n * plane;
-        const float* b = blend + n * M * plane + q;
-        float* g = gB + n * M * plane + q;
-        float bv[KMD_MAX_SIZES], d[KMD_MAX_SIZES];
-        float m = -INFINITY;
+                                                        int M, int plane) {
+    const int nq = (plane + 3) / 4;
+    const size_t f0 = (size_t)blockIdx.y * M * plane;
+    for (int t = blockIdx.x * 256 + threadIdx.x; t < nq; t += gridDim.x * 256) {
+        const int q0 = 4 * t, cnt = min(4, plane - q0);
+        float bv[KMD_MAX_SIZES][4], d[KMD_MAX_SIZES][4];
 #pragma unroll
-        for (int i = 0; i < KMD_MAX_SIZES; ++i)
-            if (i < M) {
-                bv[i] = __ldg(b + i * plane);
-                d[i] = g[i * plane];
-                m = fmaxf(m, bv[i]);
+        for (int i = 0; i < KMD_MAX_SIZES; ++i) {
+            if (i >= M) break;
+            const float* bp = blend + f0 + (size_t)i * plane + q0;
+            const float* gp = gB + f0 + (size_t)i * plane + q0;
+            if (VEC) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(bp));
+                const float4 y = *reinterpret_cast<const float4*>(gp);
+                bv[i][0] = x.x, bv[i][1] = x.y, bv[i][2] = x.z, bv[i][3] = x.w;
+                d[i][0] = y.x, d[i][1] = y.y, d[i][2] = y.z, d[i][3] = y.w;
+            } else {
+                for (int k = 0; k < 4; ++k) {
+                    bv[i][k] = k < cnt ? __ldg(bp + k) : 0.f;
+                    d[i][k] = k < cnt ? gp[k] : 0.f;
+                }
             }
-        float s = 0.f, mean = 0.f;
+        }
 #pragma unroll
-        for (int i = 0; i < KMD_MAX_SIZES; ++i)
-            if (i < M) {
-                bv[i] = expf(bv[i] - m);
-                s += bv[i];
-                mean = fmaf(bv[i], d[i], mean);
+        for (int k = 0; k < 4; ++k) {
+            float m = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < KMD_MAX_SIZES; ++i)
+                if (i < M) m = fmaxf(m, bv[i][k]);
+            float sum = 0.f, mean = 0.f;
+#pragma unroll
+            for (int i = 0; i < KMD_MAX_SIZES; ++i)
+                if (i < M) {
+                    bv[i][k] = expf(bv[i][k] - m);
+                    sum += bv[i][k];
+                    mean = fmaf(bv[i][k], d[i][k], mean);
+                }
+            const float inv = 1.f / sum;
+            mean *= inv;
+#pragma unroll
+            for (int i = 0; i < KMD_MAX_SIZES; ++i)
+                if (i < M) d[i][k] = bv[i][k] * inv * (d[i][k] - mean);
+        }
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i) {
+            if (i >= M) break;
+            float* gp = gB + f0 + (size_t)i * plane + q0;
+            if (VEC) {
+                *reinterpret_cast<float4*>(gp) = make_float4(d[i][0], d[i][1], d[i][2], d[i][3]);
+            } else {
+                for (int k = 0; k < cnt; ++k) gp[k] = d[i][k];
             }
-        const float inv = 1.f / s;
-        mean *= inv;
-#pragma unroll
-        for (int i = 0; i < KMD_MAX_SIZES; ++i)
-            if (i < M) g[i * plane] = bv[i] * inv * (d[i] - mean);
+        }
     }
 }
 
@@ -420,10 +448,12 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
     // ---- pass C: dL/dB
     if (gB && M == 1) return cudaMemsetAsync(gB, 0, sizeof(float) * (size_t)N * H * W, st);
     if (gB && logits) {
-        const long long total = (long long)N * H * W;
-        const long long need = (total + 255) / 256;
-        const int g = (int)(need < (long long)sms * 16 ? need : (long long)sms * 16);
-        bwd_blend_kernel<<<g, 256, 0, st>>>(blend, gB, N, M, (long long)H * W);
+        const int plane = H * W, nq = (plane + 3) / 4;
+        const int gx = (nq + 255) / 256 < sms * 8 ? (nq + 255) / 256 : sms * 8;
+        const dim3 grid(gx, N);
+        const bool vec = plane % 4 == 0 && (((uintptr_t)blend | (uintptr_t)gB) & 15) == 0;
+        if (vec) bwd_blend_kernel<true><<<grid, 256, 0, st>>>(blend, gB, M, plane);
+        else bwd_blend_kernel<false><<<grid, 256, 0, st>>>(blend, gB, M, plane);
         return cudaGetLastError();
     }
     return cudaSuccess;  // alpha given: dL/dalpha_i = G.R_i, written by pass A
