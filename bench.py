@@ -578,9 +578,9 @@ def run_bwd(args, rank, world, local):
                      "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / peak,
                      "algorithmic_bytes_per_launch": algo,
                      "kernel": kmd.last_kernel(),
-                     "note": f"{kmd.backward_launches_per_call(M)} launches per step (pass A: h_i and G.R_i, pass B: "
+                     "note": f"{kmd.backward_launches_per_call(M)} launches per step (pass A: s_i = a_i / den_i and d_i = G.R_i, pass B: "
                              "transposed box + dL/dI, pass C: dL/dB); algorithmic = inputs + outputs once, the "
-                             "h_i workspace (16 M B/px written and read) is not counted"},
+                             "(s_i, d_i) workspace (8 M B/px written and read) is not counted"},
         "clocks": clk.summary(), "gpu_launches": steps * kmd.backward_launches_per_call(M)}),
         flush=True)
 

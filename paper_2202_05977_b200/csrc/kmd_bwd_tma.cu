@@ -3,19 +3,20 @@
 // maps are trained end to end through Eq. 3-5).
 //
 //   pass A (kmd_tma.cu, SpecBwdH): the forward's tiles and box sums; per size i
-//          and pixel p the fusion warps write h_i(p) = (a_i G / den_i,
-//          a_i G.R_i / den_i) (a_i = softmax_i(B)(p), G = dL/dRhat(p)) to a
-//          workspace, and G.R_i(p) to grad_blend;
-//   pass B (here): T_i = Bt(h_i), the transposed clamp-to-edge box: the same
-//          warp-specialised pipeline with the field = h_i (zero outside the
-//          frame: TMA's out-of-bounds fill) and the clamped taps folded back
+//          and pixel p the fusion warps stage s_i(p) = a_i / den_i and
+//          d_i(p) = G.R_i (a_i = softmax_i(B)(p), G = dL/dRhat(p)) and TMA-store
+//          them to the workspace [N*M][2][H][W];
+//   pass B (here): T_i = Bt(h_i), h_i = s_i (G, d_i), the transposed
+//          clamp-to-edge box: the same warp-specialised pipeline, the field
+//          value h_i(q) formed from TMA boxes of (s_i, d_i) and of G (zero
+//          outside the frame: TMA's out-of-bounds fill), and the clamped taps folded back
 //          onto the border rows (field warps) and columns (fusion warps); the
 //          fusion warps finish dL/dI_i(q) = e_i(q) (r(q) . T_i.xyz - T_i.w);
 //   pass C (here): dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), elementwise.
 //
 // Pass B per CTA (one per SM), per 52 x 27 tile, per size i:
-//   warp 0       TMA: the h_i box [39][68] float4 as two 34-column halves
-//                (2-deep ring) and the I_i
+//   warp 0       TMA: the G box [3][39][68] per tile (double-buffered), the
+//                (s_i, d_i) box [2][39][68] (2-deep ring) and the I_i
 //                box [27][56] of the tile's own pixels (4-deep ring);
 //   warps 1-4    field: vertical Gil-Werman sums of h_i per column (+ folds);
 //   warps 5-11   fusion: horizontal sums (+ folds), the dL/dI epilogue.
@@ -42,15 +43,12 @@ constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;
 constexpr float LN2_HI = 0.693147182464599609375f;
 
-// h_i box: rows y0-6 .. y0+32, columns x0-8 .. x0+59 (zero outside the frame),
-// loaded as two 34-column halves (TMA boxes of 136 floats: a float4 innermost
-// dimension would make TMA move 16-byte rows); field half h reads half h only
-constexpr int HBW = 34;
-struct alignas(128) HHalf {            // 128-byte aligned: a TMA destination
-    float4 h[FH][HBW];
+// boxes: rows y0-6 .. y0+32, columns x0-8 .. x0+59, zero outside the frame
+struct alignas(128) SDSlot {
+    float sd[2][FH][BW];               // s_i = a_i / den_i and d_i = G.R_i
 };
-struct HSlot {
-    HHalf half[2];
+struct alignas(128) GBuf {
+    float g[3][FH][BW];                // dL/dRhat
 };
 struct alignas(128) Slot {
     float4 V[TH][VS];                  // Bt_y(h_i) by field column
@@ -58,12 +56,13 @@ struct alignas(128) Slot {
 struct alignas(128) ISlot {
     float I[TH][BBW];                  // I_i at the tile's pixels
 };
-static_assert(sizeof(HHalf) % 128 == 0, "TMA destinations 128-B aligned");
 struct Smem {
-    HSlot hs[NH];
+    GBuf gb[2];
+    SDSlot sd[NH];
     Slot slot[NV];
     ISlot is[NB];
-    unsigned long long h_full[NH], h_empty[NH], v_full[NV], v_empty[NV], i_full[NB], i_empty[NB];
+    unsigned long long g_full[2], g_empty[2], h_full[NH], h_empty[NH], v_full[NV], v_empty[NV], i_full[NB],
+        i_empty[NB];
 };
 
 struct BParams {
@@ -99,22 +98,25 @@ __device__ __forceinline__ float4 fma4(float m, float4 a, float4 v) {
 // folds of the clamped taps at the frame's first / last row (1-D multiplicity
 // of source s at q = 0 is R - s + 1, i.e. R - s extra; mirrored at q = H - 1)
 template <int R>
-__device__ __forceinline__ void field_job(const HSlot& hs, Slot& sl, int c, int half, int cc, int y0, int H) {
-    const float4(&hh)[FH][HBW] = hs.half[half].h;
-    const float4* hb = &hh[RMAX - R][cc];
+__device__ __forceinline__ void field_job(const SDSlot& sd, const GBuf& gb, Slot& sl, int c, int cc, int y0, int H) {
+    // h(q) = s(q) (G(q), d(q)) at box row r of this lane's column
+    auto hv = [&](int r) {
+        const float sv = sd.sd[0][r][cc];
+        return make_float4(sv * gb.g[0][r][cc], sv * gb.g[1][r][cc], sv * gb.g[2][r][cc], sv * sd.sd[1][r][cc]);
+    };
     float4* Vc = &sl.V[0][c];
-    gw_line_field<R, TH>([&](int f) { return hb[f * HBW]; }, [&](int oy, float4 v) { Vc[oy * VS] = v; });
+    gw_line_field<R, TH>([&](int f) { return hv(RMAX - R + f); }, [&](int oy, float4 v) { Vc[oy * VS] = v; });
     // folds of the clamped taps, only in the frame's first / last tile row (kept
     // out of the Gil-Werman emits: inlining them there bloated the hot code)
     if (y0 == 0) {
         float4 v = Vc[0];
-        for (int s = 0; s < R && s < H; ++s) v = fma4((float)(R - s), hh[RMAX + s][cc], v);
+        for (int s = 0; s < R && s < H; ++s) v = fma4((float)(R - s), hv(RMAX + s), v);
         Vc[0] = v;
     }
     if (H - 1 - y0 < TH) {
         const int oy = H - 1 - y0;
         float4 v = Vc[oy * VS];
-        for (int s = max(H - R, 0); s < H; ++s) v = fma4((float)(s + R - H + 1), hh[RMAX + s - y0][cc], v);
+        for (int s = max(H - R, 0); s < H; ++s) v = fma4((float)(s + R - H + 1), hv(RMAX + s - y0), v);
         Vc[oy * VS] = v;
     }
 }
@@ -126,13 +128,18 @@ __device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-    bwd_t_kernel(const __grid_constant__ BParams p, const __grid_constant__ CUtensorMap tm_h,
-                 const __grid_constant__ CUtensorMap tm_i, int tiles_x, int tiles_y, int n_tiles) {
+    bwd_t_kernel(const __grid_constant__ BParams p, const __grid_constant__ CUtensorMap tm_sd,
+                 const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_i, int tiles_x,
+                 int tiles_y, int n_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = p.M;
     if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sm.g_full[b], 1);
+            mbar_init(&sm.g_empty[b], NFIELD);
+        }
         for (int s = 0; s < NH; ++s) {
             mbar_init(&sm.h_full[s], 1);
             mbar_init(&sm.h_empty[s], 2);
@@ -163,14 +170,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int tl = 0; tl < my_tiles; ++tl) {
                 int n, x0, y0;
                 tile(tl, n, x0, y0);
+                const int gbi = tl & 1;
+                mbar_wait(&sm.g_empty[gbi], ((tl >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.g_full[gbi], 3 * FH * BW * 4);
+                tma_load_3d(&sm.gb[gbi].g[0][0][0], &tm_g, x0 - XOFF, y0 - RMAX, 3 * n, &sm.g_full[gbi]);
                 for (int i = 0; i < M; ++i) {
                     const int seq = tl * M + i, sh = seq % NH, sb = seq % NB;
                     mbar_wait(&sm.h_empty[sh], ((seq / NH) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&sm.h_full[sh], 2 * FH * HBW * 16);
-                    tma_load_3d(&sm.hs[sh].half[0].h[0][0], &tm_h, 4 * (x0 - XOFF), y0 - RMAX, n * M + i,
-                                &sm.h_full[sh]);
-                    tma_load_3d(&sm.hs[sh].half[1].h[0][0], &tm_h, 4 * (x0 - XOFF + HBW), y0 - RMAX, n * M + i,
-                                &sm.h_full[sh]);
+                    mbar_arrive_expect_tx(&sm.h_full[sh], 2 * FH * BW * 4);
+                    tma_load_3d(&sm.sd[sh].sd[0][0][0], &tm_sd, x0 - XOFF, y0 - RMAX, 2 * (n * M + i), &sm.h_full[sh]);
                     mbar_wait(&sm.i_empty[sb], ((seq / NB) & 1) ^ 1);
                     mbar_arrive_expect_tx(&sm.i_full[sb], TH * BBW * 4);
                     tma_load_3d(&sm.is[sb].I[0][0], &tm_i, x0, y0, n * M + i, &sm.i_full[sb]);
@@ -183,23 +191,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int n, x0, y0;
             tile(tl, n, x0, y0);
             (void)n;
+            const int gbi = tl & 1;
+            mbar_wait(&sm.g_full[gbi], (tl >> 1) & 1);
 #pragma unroll 1
             for (int jl = fw; jl < 2 * M; jl += NFIELD) {
                 const int i = jl >> 1, h = jl & 1;
                 const int seq = tl * M + i, sh = seq % NH, sv = seq % NV;
-                // field column c <-> global x0 - 6 + c <-> column c + 2 - 34 h of half h
+                // field column c <-> global x0 - 6 + c <-> box column c + 2
                 // (unclamped: zero outside the frame)
-                const int c = h * 32 + lane, cc = c + XOFF - RMAX - HBW * h;
+                const int c = h * 32 + lane, cc = c + XOFF - RMAX;
                 mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1);
                 mbar_wait(&sm.h_full[sh], (seq / NH) & 1);
+                const SDSlot& sd = sm.sd[sh];
+                const GBuf& gb = sm.gb[gbi];
                 switch ((p.rpack >> (4 * i)) & 15) {
-                    case 0: field_job<0>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    case 1: field_job<1>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    case 2: field_job<2>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    case 3: field_job<3>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    case 4: field_job<4>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    case 5: field_job<5>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
-                    default: field_job<6>(sm.hs[sh], sm.slot[sv], c, h, cc, y0, p.H); break;
+                    case 0: field_job<0>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    case 1: field_job<1>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    case 2: field_job<2>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    case 3: field_job<3>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    case 4: field_job<4>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    case 5: field_job<5>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
+                    default: field_job<6>(sd, gb, sm.slot[sv], c, cc, y0, p.H); break;
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -207,6 +219,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_arrive(&sm.v_full[sv]);
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.g_empty[gbi]);
         }
     } else {
         const int c = threadIdx.x - (1 + NFIELD) * 32;
@@ -284,8 +298,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // One thread per 4 consecutive pixels of a frame (float4 when plane % 4 == 0);
 // blockIdx.y = frame, so no 64-bit division per element.
 template <bool VEC>
-__global__ void __launch_bounds__(256) bwd_blend_kernel(const float* __restrict__ blend, float* __restrict__ gB,
-                                                        int M, int plane) {
+__global__ void __launch_bounds__(256) bwd_blend_kernel(const float* __restrict__ blend, const float* __restrict__ ws,
+                                                        float* __restrict__ gB, int M, int plane) {
     const int nq = (plane + 3) / 4;
     const size_t f0 = (size_t)blockIdx.y * M * plane;
     for (int t = blockIdx.x * 256 + threadIdx.x; t < nq; t += gridDim.x * 256) {
@@ -295,16 +309,16 @@ __global__ void __launch_bounds__(256) bwd_blend_kernel(const float* __restrict_
         for (int i = 0; i < KMD_MAX_SIZES; ++i) {
             if (i >= M) break;
             const float* bp = blend + f0 + (size_t)i * plane + q0;
-            const float* gp = gB + f0 + (size_t)i * plane + q0;
+            const float* gp = ws + 2 * (f0 + (size_t)i * plane) + plane + q0;  // d_i of [N*M][2][H][W]
             if (VEC) {
                 const float4 x = __ldg(reinterpret_cast<const float4*>(bp));
-                const float4 y = *reinterpret_cast<const float4*>(gp);
+                const float4 y = __ldg(reinterpret_cast<const float4*>(gp));
                 bv[i][0] = x.x, bv[i][1] = x.y, bv[i][2] = x.z, bv[i][3] = x.w;
                 d[i][0] = y.x, d[i][1] = y.y, d[i][2] = y.z, d[i][3] = y.w;
             } else {
                 for (int k = 0; k < 4; ++k) {
                     bv[i][k] = k < cnt ? __ldg(bp + k) : 0.f;
-                    d[i][k] = k < cnt ? gp[k] : 0.f;
+                    d[i][k] = k < cnt ? __ldg(gp + k) : 0.f;
                 }
             }
         }
@@ -379,14 +393,15 @@ bool bwd_tma_supported(int H, int W, int M, const int* sizes, const void* a, con
     return bwd::get_encode() != nullptr;
 }
 
-size_t bwd_tma_workspace_bytes(int N, int H, int W, int M) { return (size_t)N * M * H * W * sizeof(float4); }
+// (s_i, d_i) per pixel and size: [N*M][2][H][W] floats
+size_t bwd_tma_workspace_bytes(int N, int H, int W, int M) { return (size_t)N * M * H * W * 2 * sizeof(float); }
 
 cudaError_t launch_backward_tma(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
                                 float* gB, int N, int H, int W, int M, const int* sizes, int logits, void* ws,
                                 cudaStream_t st) {
     using namespace bwd;
-    float4* hbuf = reinterpret_cast<float4*>(ws);
-    // ---- pass A: h_i and G.R_i (the forward kernel's tiles and box sums)
+    float* sd = reinterpret_cast<float*>(ws);
+    // ---- pass A: (s_i, d_i) (the forward kernel's tiles and box sums)
     FusedParams p{};
     p.rad = rad;
     p.imp = imp;
@@ -410,21 +425,24 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
     }
     p.rmax = rmax;
     p.grad = G;
-    p.hbuf = hbuf;
-    p.dotbuf = M > 1 ? gB : nullptr;
     static const int dbg = [] { const char* s = getenv("KMD_DEBUG"); return s ? atoi(s) : 0; }();
     p.debug = dbg;
-    cudaError_t e = launch_bwd_h_tma(p, st);
+    cudaError_t e = launch_bwd_h_tma(p, sd, st);
     if (e != cudaSuccess) return e;
-    // ---- pass B: transposed box of h_i, dL/dI_i
+    // ---- pass B: transposed box of h_i = s_i (G, d_i), dL/dI_i
     BParams q{rad, imp, gI, N, H, W, M, rpack, dbg};
-    CUtensorMap m_h, m_i;
+    CUtensorMap m_sd, m_g, m_i;
     {
-        // h as a 3-D [N*M][H][4W] float array; boxes of 34 float4 = 136 floats
-        const cuuint64_t dims[3] = {4 * (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N * M};
-        const cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)W * H * 16};
-        const cuuint32_t box[3] = {4 * HBW, FH, 1};
-        if (!encode(&m_h, 3, hbuf, dims, strides, box)) return cudaErrorInvalidValue;
+        const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, 2 * (cuuint64_t)N * M};
+        const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+        const cuuint32_t box[3] = {BW, FH, 2};
+        if (!encode(&m_sd, 3, sd, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, 3 * (cuuint64_t)N};
+        const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+        const cuuint32_t box[3] = {BW, FH, 3};
+        if (!encode(&m_g, 3, G, dims, strides, box)) return cudaErrorInvalidValue;
     }
     {
         const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N * M};
@@ -443,7 +461,7 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
         cudaSuccess)
         return e;
     const int grid = (int)(n_tiles < sms ? n_tiles : sms);
-    bwd_t_kernel<<<grid, NTHREADS, smem, st>>>(q, m_h, m_i, tiles_x, tiles_y, (int)n_tiles);
+    bwd_t_kernel<<<grid, NTHREADS, smem, st>>>(q, m_sd, m_g, m_i, tiles_x, tiles_y, (int)n_tiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // ---- pass C: dL/dB
     if (gB && M == 1) return cudaMemsetAsync(gB, 0, sizeof(float) * (size_t)N * H * W, st);
@@ -452,11 +470,14 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
         const int gx = (nq + 255) / 256 < sms * 8 ? (nq + 255) / 256 : sms * 8;
         const dim3 grid(gx, N);
         const bool vec = plane % 4 == 0 && (((uintptr_t)blend | (uintptr_t)gB) & 15) == 0;
-        if (vec) bwd_blend_kernel<true><<<grid, 256, 0, st>>>(blend, gB, M, plane);
-        else bwd_blend_kernel<false><<<grid, 256, 0, st>>>(blend, gB, M, plane);
+        if (vec) bwd_blend_kernel<true><<<grid, 256, 0, st>>>(blend, sd, gB, M, plane);
+        else bwd_blend_kernel<false><<<grid, 256, 0, st>>>(blend, sd, gB, M, plane);
         return cudaGetLastError();
     }
-    return cudaSuccess;  // alpha given: dL/dalpha_i = G.R_i, written by pass A
+    if (gB)  // alpha given: dL/dalpha_i = G.R_i = d_i, every second plane of the workspace
+        return cudaMemcpy2DAsync(gB, (size_t)H * W * 4, sd + (size_t)H * W, 2 * (size_t)H * W * 4,
+                                 (size_t)H * W * 4, (size_t)N * M, cudaMemcpyDeviceToDevice, st);
+    return cudaSuccess;
 }
 
 }  // namespace kmd

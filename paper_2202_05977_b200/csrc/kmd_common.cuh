@@ -29,10 +29,9 @@ struct FusedParams {
     int blend_is_logits;
     int sizes[KMD_MAX_SIZES];
     int debug;           // development switches (env KMD_DEBUG); 0 in production
-    // backward pass A (kmd_bwd_tma.cu): dL/dRhat in, per-size gradient field out
+    // backward pass A (kmd_bwd_tma.cu): dL/dRhat in; per size i the pair
+    // (a_i / den_i, G.R_i) out through the stage buffer and tm_out
     const float* grad;   // [N,3,H,W] or nullptr
-    float4* hbuf;        // [N,M,H,W] h_i = (a G / den, a G.R_i / den) or nullptr
-    float* dotbuf;       // [N,M,H,W] G.R_i or nullptr
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }

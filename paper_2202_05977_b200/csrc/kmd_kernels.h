@@ -30,7 +30,7 @@ cudaError_t launch_combine(const float* fine, const float* coarse, const float* 
 
 // backward (NEXT row 3): pass A in kmd_tma.cu (h_i, G.R_i), pass B / C in
 // kmd_bwd_tma.cu, the one-launch fallback in kmd_bwd.cu
-cudaError_t launch_bwd_h_tma(FusedParams p, cudaStream_t stream);
+cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream);
 bool bwd_tma_supported(int H, int W, int M, const int* sizes, const void* a, const void* b, const void* c,
                        const void* d);
 size_t bwd_tma_workspace_bytes(int N, int H, int W, int M);

@@ -548,7 +548,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int i = 0; i < M; ++i) {
                     IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                     if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                    if (active && !(p.debug & 64)) {
+                    // (a_i / den_i, G.R_i) of this thread's pixels
+                    float sv[SEG], dv[SEG];
+                    if (active) {
                         float4 o[SEG];
                         switch ((rpack >> (4 * i)) & 15) {
                             case 0: hbox<0>(sm.slot[vs], ty, xs, o); break;
@@ -560,30 +562,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             default: hbox<6>(sm.slot[vs], ty, xs, o); break;
                         }
                         const float* Br = &sm.bl[bs].B[ty][xs];
-                        const size_t base = ((size_t)tc.n * M + i) * plane + (size_t)gyc * p.W;
 #pragma unroll
                         for (int j = 0; j < SEG; ++j) {
-                            const int gx = tc.x0 + xs + j;
-                            if (j < len && row_ok && gx < p.W && !(p.debug & 1)) {
-                                const float rden = rcp_approx(o[j].x);
-                                const float R0 = o[j].y * rden, R1 = o[j].z * rden, R2 = o[j].w * rden;
-                                const float a = M == 1 ? 1.f : (logits ? exp_acc(Br[j] - mb[j]) * is[j] : Br[j]);
-                                const float dot = fmaf(G[j][0], R0, fmaf(G[j][1], R1, G[j][2] * R2));
-                                const float ar = a * rden;
-                                p.hbuf[base + gx] = make_float4(ar * G[j][0], ar * G[j][1], ar * G[j][2], ar * dot);
-                                if (p.dotbuf) p.dotbuf[base + gx] = dot;
-                            }
+                            const float rden = rcp_approx(o[j].x);
+                            const float R0 = o[j].y * rden, R1 = o[j].z * rden, R2 = o[j].w * rden;
+                            const float a = M == 1 ? 1.f : (logits ? exp_acc(Br[j] - mb[j]) * is[j] : Br[j]);
+                            sv[j] = a * rden;
+                            dv[j] = fmaf(G[j][0], R0, fmaf(G[j][1], R1, G[j][2] * R2));
                         }
                     }
                     __syncwarp();
-                    if ((c & 31) == 0) {
+                    if ((c & 31) == 0) {  // V and the logits are consumed: release them now
                         mbar_arrive(&sm.v_empty[vs]);
                         if (has_blend) mbar_arrive(&sm.b_empty[bs]);
                     }
+                    // the stage is free once the previous size's store has read it
+                    if (c == 0) bulk_wait_read0();
+                    fuse_bar();
+                    if (active) {
+#pragma unroll
+                        for (int j = 0; j < SEG; ++j)
+                            if (j < len) {
+                                sm.stage[0][ty][xs + j] = sv[j];
+                                sm.stage[1][ty][xs + j] = dv[j];
+                            }
+                    }
+                    fence_proxy_async();
+                    fuse_bar();
+                    // one TMA store of the pair of planes [2][27][52] (clipped at the frame edge)
+                    if (c == 0 && !(p.debug & 1))
+                        tma_store_3d(&tm_out, tc.x0, tc.y0, 2 * (tc.n * M + i), &sm.stage[0][0][0]);
                     if (++vs == NV) { vs = 0; vph ^= 1; }
                     if (++bs == NB) { bs = 0; bph ^= 1; }
                 }
                 continue;
+
             }
             // albedo of this thread's pixels, loaded now so the latency hides
             // behind the M sizes (remodulation epilogue)
@@ -726,8 +739,9 @@ extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
 }
 #endif
 
-// backward pass A (NEXT row 3, kmd_bwd_tma.cu): whole frames only
-cudaError_t launch_bwd_h_tma(FusedParams p, cudaStream_t stream) {
+// backward pass A (NEXT row 3, kmd_bwd_tma.cu): whole frames only; the pairs
+// (a_i / den_i, G.R_i) go to ws as [N*M][2][H][W]
+cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream) {
     using namespace tma;
     p.tile_y_begin = 0;
     const int tiles_y = (p.H + TH - 1) / TH, tiles_x = (p.W + TW - 1) / TW;
@@ -735,14 +749,14 @@ cudaError_t launch_bwd_h_tma(FusedParams p, cudaStream_t stream) {
     if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
     CUtensorMap m_rad, m_imp, m_blend, m_out;
     if (!make_map(&m_rad, p.rad, p.W, p.H, 3LL * p.N, BW, FH, 3) ||
-        !make_map(&m_imp, p.imp, p.W, p.H, (long long)p.M * p.N, BW, FH, 1))
+        !make_map(&m_imp, p.imp, p.W, p.H, (long long)p.M * p.N, BW, FH, 1) ||
+        !make_map(&m_out, ws, p.W, p.H, 2LL * p.M * p.N, TW, TH, 2))
         return cudaErrorInvalidValue;
     if (p.blend) {
         if (!make_map(&m_blend, p.blend, p.W, p.H, (long long)p.M * p.N, BBW, TH, 1)) return cudaErrorInvalidValue;
     } else {
         m_blend = m_imp;
     }
-    m_out = m_rad;  // no store
     int dev = 0, sms = 148;
     cudaError_t err = cudaGetDevice(&dev);
     if (err != cudaSuccess) return err;
