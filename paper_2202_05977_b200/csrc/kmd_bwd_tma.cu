@@ -37,7 +37,7 @@ constexpr int RMAX = 6;
 constexpr int TW = 52, TH = 27, FH = TH + 2 * RMAX;  // 39 field rows
 constexpr int XOFF = 8, BW = 68, VS = 68, BBW = 56;
 constexpr int SEG = 7, NSEG = 8;
-constexpr int NH = 2, NB = 4, NV = 3;
+constexpr int NH = 2, NB = 2, NV = 3;
 constexpr int NFIELD = 4, NFUSE = (TH * NSEG + 31) / 32;  // 7
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;
@@ -56,11 +56,15 @@ struct alignas(128) Slot {
 struct alignas(128) ISlot {
     float I[TH][BBW];                  // I_i at the tile's pixels
 };
+struct alignas(128) GStage {
+    float g[TH][TW];                   // dL/dI_i of the tile, TMA-stored
+};
 struct Smem {
     GBuf gb[2];
     SDSlot sd[NH];
     Slot slot[NV];
     ISlot is[NB];
+    GStage st[2];
     unsigned long long g_full[2], g_empty[2], h_full[NH], h_empty[NH], v_full[NV], v_empty[NV], i_full[NB],
         i_empty[NB];
 };
@@ -89,6 +93,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
 
 __device__ __forceinline__ float4 fma4(float m, float4 a, float4 v) {
     return make_float4(fmaf(m, a.x, v.x), fmaf(m, a.y, v.y), fmaf(m, a.z, v.z), fmaf(m, a.w, v.w));
@@ -129,8 +143,8 @@ __device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     bwd_t_kernel(const __grid_constant__ BParams p, const __grid_constant__ CUtensorMap tm_sd,
-                 const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_i, int tiles_x,
-                 int tiles_y, int n_tiles) {
+                 const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_i,
+                 const __grid_constant__ CUtensorMap tm_gi, int tiles_x, int tiles_y, int n_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -229,7 +243,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
         const int len = (0x76677766u >> (4 * sub)) & 0xf;
         const size_t plane = (size_t)p.H * p.W;
-        int vs = 0, vph = 0, bs = 0, bph = 0;
+        int vs = 0, vph = 0, bs = 0, bph = 0, sb2 = 0;
         for (int tl = 0; tl < my_tiles; ++tl) {
             int n, x0, y0;
             tile(tl, n, x0, y0);
@@ -263,13 +277,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         default: hbox<6>(sl, ty, xs, o); break;
                     }
                     const float* Ir = &sm.is[bs].I[ty][xs];
-                    float* go = p.gI + ((size_t)n * M + i) * plane + (size_t)gyc * p.W;
+                    float* go = &sm.st[sb2].g[ty][xs];
 #pragma unroll
                     for (int j = 0; j < SEG; ++j) {
                         const int gx = x0 + xs + j;
-                        if (j < len && row_ok && gx < p.W && !(p.debug & 1)) {
+                        if (j < len) {
                             float4 v = o[j];
-                            if (edge_x) {  // horizontal folds at the frame's first / last column
+                            if (edge_x && row_ok) {  // horizontal folds at the frame's first / last column
                                 if (gx == 0)
                                     for (int s = 0; s < R && s < p.W; ++s)
                                         v = fma4((float)(R - s), sl.V[ty][s - x0 + RMAX], v);
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                         v = fma4((float)(s + R - p.W + 1), sl.V[ty][s - x0 + RMAX], v);
                             }
                             const float e = exp_acc(Ir[j]);
-                            go[gx] = e * (fmaf(rr[j][0], v.x, fmaf(rr[j][1], v.y, rr[j][2] * v.z)) - v.w);
+                            go[j] = e * (fmaf(rr[j][0], v.x, fmaf(rr[j][1], v.y, rr[j][2] * v.z)) - v.w);
                         }
                     }
                 }
@@ -287,10 +301,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_arrive(&sm.v_empty[vs]);
                     mbar_arrive(&sm.i_empty[bs]);
                 }
+                // the tile's dL/dI_i leaves with one TMA store (clipped at the frame
+                // edge); double-buffered stage: before the barrier, the store of
+                // the previous step must have read its buffer (reused next step)
+                fence_proxy_async();
+                if (c == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                fuse_bar();
+                if (c == 0 && !(p.debug & 1)) tma_store_3d(&tm_gi, x0, y0, n * M + i, &sm.st[sb2].g[0][0]);
+                sb2 ^= 1;
                 if (++vs == NV) { vs = 0; vph ^= 1; }
                 if (++bs == NB) { bs = 0; bph ^= 1; }
             }
         }
+        if (c == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
 }
 
@@ -444,11 +467,14 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
         const cuuint32_t box[3] = {BW, FH, 3};
         if (!encode(&m_g, 3, G, dims, strides, box)) return cudaErrorInvalidValue;
     }
+    CUtensorMap m_gi;
     {
         const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N * M};
         const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
         const cuuint32_t box[3] = {BBW, TH, 1};
         if (!encode(&m_i, 3, imp, dims, strides, box)) return cudaErrorInvalidValue;
+        const cuuint32_t obox[3] = {TW, TH, 1};
+        if (!encode(&m_gi, 3, gI, dims, strides, obox)) return cudaErrorInvalidValue;
     }
     const int tiles_y = (H + TH - 1) / TH, tiles_x = (W + TW - 1) / TW;
     const long long n_tiles = (long long)tiles_x * tiles_y * N;
@@ -461,7 +487,7 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
         cudaSuccess)
         return e;
     const int grid = (int)(n_tiles < sms ? n_tiles : sms);
-    bwd_t_kernel<<<grid, NTHREADS, smem, st>>>(q, m_sd, m_g, m_i, tiles_x, tiles_y, (int)n_tiles);
+    bwd_t_kernel<<<grid, NTHREADS, smem, st>>>(q, m_sd, m_g, m_i, m_gi, tiles_x, tiles_y, (int)n_tiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // ---- pass C: dL/dB
     if (gB && M == 1) return cudaMemsetAsync(gB, 0, sizeof(float) * (size_t)N * H * W, st);
