@@ -14,7 +14,7 @@
 // HBM-bound (94 B/px).  Each thread owns 4 consecutive pixels of a row so the
 // coalesced streams (current buffers, motion, outputs) move as 16-byte
 // vectors when W % 4 == 0; the previous-frame reads are gathers (coherent for
-// smooth motion).  Grid-stride over (frame, row, quad) with a grid of a few
+// smooth motion), all issued together right after the reprojection.  Grid-stride over (frame, row, quad) with a grid of a few
 // CTAs per SM.
 #include "kmd_kernels.h"
 
@@ -63,27 +63,45 @@ __global__ void __launch_bounds__(256) temporal_kernel(const TParams t) {
             load4<VEC>(t.cur_pos + f3 + c * plane + p0, cp[c], cnt);
             load4<VEC>(t.cur_nrm + f3 + c * plane + p0, cn[c], cnt);
         }
+        // reproject all four pixels, then issue every gather at once (validity,
+        // previous position / normal / radiance): one dependent load level
+        // after the motion vectors instead of three
+        size_t sidx[4];
+        bool inb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            // nearest pixel in fp32 (reading R21)
+            const float fx = floorf(__fadd_rn(__fadd_rn((float)(x0 + j), mx[j]), 0.5f));
+            const float fy = floorf(__fadd_rn(__fadd_rn((float)y, my[j]), 0.5f));
+            inb[j] = j < cnt && fx >= 0.f && fx <= (float)(t.W - 1) && fy >= 0.f && fy <= (float)(t.H - 1);
+            sidx[j] = inb[j] ? (size_t)(int)fy * t.W + (size_t)(int)fx : 0;
+        }
+        unsigned char pv[4];
+        float pp[3][4], pn[3][4], pr[3][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const size_t s = sidx[j];
+            pv[j] = inb[j] ? __ldg(t.prev_valid + (size_t)n * plane + s) : 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                pp[c][j] = inb[j] ? __ldg(t.prev_pos + f3 + c * plane + s) : 0.f;
+                pn[c][j] = inb[j] ? __ldg(t.prev_nrm + f3 + c * plane + s) : 0.f;
+                pr[c][j] = inb[j] ? __ldg(t.prev_rad + f3 + c * plane + s) : 0.f;
+            }
+        }
         float out[3][4];
         unsigned char mk[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            // reproject: nearest pixel in fp32 (reading R21)
-            const float fx = floorf(__fadd_rn(__fadd_rn((float)(x0 + j), mx[j]), 0.5f));
-            const float fy = floorf(__fadd_rn(__fadd_rn((float)y, my[j]), 0.5f));
-            bool m = j < cnt && fx >= 0.f && fx <= (float)(t.W - 1) && fy >= 0.f && fy <= (float)(t.H - 1);
-            size_t s = 0;
-            if (m) {
-                s = (size_t)(int)fy * t.W + (size_t)(int)fx;
-                m = __ldg(t.prev_valid + (size_t)n * plane + s) != 0;
-            }
+            bool m = inb[j] && pv[j] != 0;
             if (m) {
                 // consistency test, fp32, fixed order (reading R22)
                 float d[3], a[3], b[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    d[c] = __fsub_rn(cp[c][j], __ldg(t.prev_pos + f3 + c * plane + s));
+                    d[c] = __fsub_rn(cp[c][j], pp[c][j]);
                     a[c] = __fsub_rn(__fmul_rn(2.f, cn[c][j]), 1.f);
-                    b[c] = __fsub_rn(__fmul_rn(2.f, __ldg(t.prev_nrm + f3 + c * plane + s)), 1.f);
+                    b[c] = __fsub_rn(__fmul_rn(2.f, pn[c][j]), 1.f);
                 }
                 const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(d[0], d[0]), __fmul_rn(d[1], d[1])), __fmul_rn(d[2], d[2]));
                 const float dot = __fadd_rn(__fadd_rn(__fmul_rn(a[0], b[0]), __fmul_rn(a[1], b[1])), __fmul_rn(a[2], b[2]));
@@ -93,9 +111,7 @@ __global__ void __launch_bounds__(256) temporal_kernel(const TParams t) {
             }
             mk[j] = m ? 1 : 0;
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                out[c][j] = m ? fmaf(t.alpha, cr[c][j], (1.f - t.alpha) * __ldg(t.prev_rad + f3 + c * plane + s))
-                              : cr[c][j];
+            for (int c = 0; c < 3; ++c) out[c][j] = m ? fmaf(t.alpha, cr[c][j], (1.f - t.alpha) * pr[c][j]) : cr[c][j];
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
