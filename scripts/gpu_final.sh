@@ -1,0 +1,15 @@
+# usage: bash scripts/gpu_final.sh TAG -- the round's evidence: tests, the default bench line,
+# every other bench mode, the launch list and one ncu --set full capture of the hot kernel
+TAG=${1:-final}
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
+timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
+for m in "--albedo" "--mode mr" "--mode band" "--mode bwd" "--mode temporal" "--mode sweep" "--mode batch" "--impl reference --steps 3 --warmup 3"; do
+  n=$(echo $m | tr -d ' -' )
+  timeout 600 python bench.py $m 2>&1 | grep '^{' | tail -1 > gpurun_out/bench_${TAG}_$n.json
+done
+CMD="python bench.py --steps 16 --warmup 8 --no-cpu-baseline --e2e-steps 0"
+timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fused -c 40 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -s 8 -c 1 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_full_$TAG.log
