@@ -514,8 +514,8 @@ def run_mr(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": measured_peak_hbm()[0],
                      "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / measured_peak_hbm()[0],
                      "algorithmic_bytes_per_launch": algo,
-                     "note": "7 launches per step (2 downsample, 3 fused, 2 combine); algorithmic = inputs + output once"},
-        "clocks": clk.summary(), "gpu_launches": steps * 7,
+                     "note": "6 launches per step (one 2-level downsample, 3 fused, 2 combine); algorithmic = inputs + output once"},
+        "clocks": clk.summary(), "gpu_launches": steps * 6,
         "paper_context": "Ours MR reconstruction 0.85 ms at 1280x720 on an RTX 2080 Ti (PAPER.md:435)"}),
         flush=True)
 

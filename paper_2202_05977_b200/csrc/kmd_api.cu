@@ -504,7 +504,13 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
     }
     r[0] = const_cast<float*>(radiance);
     cudaError_t e;
-    for (int l = 1; l < L; ++l)
+    int l0 = 1;
+    if (L >= 3) {  // levels 1 and 2 in one pass over the frame
+        if ((e = kmd::launch_down4(r[0], r[1], r[2], N * 3, H >> 2, W >> 2, st)) != cudaSuccess)
+            return cuda_fail(e, "downsample launch");
+        l0 = 3;
+    }
+    for (int l = l0; l < L; ++l)
         if ((e = kmd::launch_down2(r[l - 1], r[l], (long long)N * 3, H >> l, W >> l, st)) != cudaSuccess)
             return cuda_fail(e, "downsample launch");
     for (int l = 0; l < L; ++l) {

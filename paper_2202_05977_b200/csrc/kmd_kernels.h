@@ -25,6 +25,7 @@ cudaError_t launch_albedo_op(const float* x, const float* albedo, float eps, flo
 
 // multi-resolution ("Ours MR", NEXT row 2; kmd_mr.cu)
 cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, int Wo, cudaStream_t st);
+cudaError_t launch_down4(const float* in, float* out1, float* out2, int planes, int H2, int W2, cudaStream_t st);
 cudaError_t launch_combine(const float* fine, const float* coarse, const float* alpha, float* out, int N, int H,
                            int W, cudaStream_t st);
 

@@ -41,6 +41,45 @@ __global__ void __launch_bounds__(256) down2_kernel(const float* __restrict__ in
     }
 }
 
+// Two pyramid levels in one pass: each thread reads a 4x4 block of the fine
+// plane and writes its 2x2 block of level 1 and the level-2 pixel, each the
+// 2x2 mean of the level below in the same fp32 order as down2_kernel (so the
+// bits equal two down2 passes).  H0, W0 divisible by 4.
+template <bool VEC>
+__global__ void __launch_bounds__(256) down4_kernel(const float* __restrict__ in, float* __restrict__ out1,
+                                                    float* __restrict__ out2, int planes, int H2, int W2) {
+    const int W0 = 4 * W2, W1 = 2 * W2;
+    const long long total = (long long)planes * H2 * W2;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int pl = (int)(t / ((long long)H2 * W2));
+        const int r = (int)(t - (long long)pl * H2 * W2), y = r / W2, x = r - y * W2;
+        const float* s = in + ((size_t)pl * 4 * H2 + 4 * y) * W0 + 4 * x;
+        float v[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (VEC) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(s + (size_t)k * W0));
+                v[k][0] = q.x, v[k][1] = q.y, v[k][2] = q.z, v[k][3] = q.w;
+            } else {
+                for (int m = 0; m < 4; ++m) v[k][m] = __ldg(s + (size_t)k * W0 + m);
+            }
+        }
+        float l1[2][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+                l1[a][b] = 0.25f * ((v[2 * a][2 * b] + v[2 * a][2 * b + 1]) + (v[2 * a + 1][2 * b] + v[2 * a + 1][2 * b + 1]));
+        float* o1 = out1 + ((size_t)pl * 2 * H2 + 2 * y) * W1 + 2 * x;
+        o1[0] = l1[0][0];
+        o1[1] = l1[0][1];
+        o1[W1] = l1[1][0];
+        o1[W1 + 1] = l1[1][1];
+        out2[((size_t)pl * H2 + y) * W2 + x] = 0.25f * ((l1[0][0] + l1[0][1]) + (l1[1][0] + l1[1][1]));
+    }
+}
+
 // Eq. 7: o = f - alpha * [U D f] + alpha * [U c], computed as
 // fma(alpha, Uc - UDf, f).  One thread per 2x2 block of fine pixels and all
 // three channels: the block's D f, the one coarse value and the 2x2 alphas are
@@ -94,6 +133,16 @@ cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, 
     const long long n = planes * Ho * ((Wo + 1) / 2);
     if (n == 0) return cudaSuccess;
     down2_kernel<<<grid_for(n), 256, 0, st>>>(in, out, planes, Ho, Wo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_down4(const float* in, float* out1, float* out2, int planes, int H2, int W2, cudaStream_t st) {
+    const long long n = (long long)planes * H2 * W2;
+    if (n == 0) return cudaSuccess;
+    if (((uintptr_t)in & 15) == 0)
+        down4_kernel<true><<<grid_for(n), 256, 0, st>>>(in, out1, out2, planes, H2, W2);
+    else
+        down4_kernel<false><<<grid_for(n), 256, 0, st>>>(in, out1, out2, planes, H2, W2);
     return cudaGetLastError();
 }
 
