@@ -354,10 +354,15 @@ def run_kmd(args, rank, world, local):
         rows, _ = calibrate_rows(inp_cpu, sizes, H, args.cpu_seconds)
         y0 = max(0, (H - rows) // 2)
         dt, ref = oracle_rows_time(inp_cpu, sizes, (y0, y0 + rows))
+        # and one thread on a few rows (the per-core figure)
+        r1 = max(1, min(8, rows))
+        dt1, _ = oracle_rows_time(inp_cpu, sizes, (y0, y0 + r1), threads=1)
         cpu = {"value": rows * W / dt / 1e6, "unit": UNIT, "cores": oracle.max_threads(),
                "kind": "oracle",
                "sample": f"rows {y0}..{y0 + rows} ({rows * W} px) of frame 0 of the {W}x{H} "
-                         f"M={M} workload, fp64 oracle, {dt:.1f} s"}
+                         f"M={M} workload, fp64 oracle, {dt:.1f} s",
+               "value_1thread": r1 * W / dt1 / 1e6,
+               "sample_1thread": f"rows {y0}..{y0 + r1} ({r1 * W} px), one thread, {dt1:.2f} s"}
         r0, i0, b0, o0, a0 = views[0]
         kmd.decode_filter_fuse(r0, i0, b0, sizes, out=o0, stream=stream)
         torch.cuda.synchronize(dev)
