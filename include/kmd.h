@@ -174,7 +174,10 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
  *   blend[l]      [N,M_l,H>>l,W>>l] or NULL iff M_l == 1
  *   alpha[l]      [N,1,H>>l,W>>l], l < levels-1  Eq. 7 blending weight in [0,1]
  *   out           [N,3,H,W]
- *   workspace     device scratch of kmd_mr_workspace_bytes(...) bytes        */
+ *   workspace     device scratch of kmd_mr_workspace_bytes(...) bytes
+ * The coarse levels run on a library-owned auxiliary stream (thread-local,
+ * created on first use) forked from and joined back into `stream`, so the
+ * call stays ordered on `stream` (and capturable into a CUDA graph).        */
 #define KMD_MR_MAX_LEVELS 4
 typedef struct {
     int32_t levels;                          /* 1..KMD_MR_MAX_LEVELS (paper: 3) */

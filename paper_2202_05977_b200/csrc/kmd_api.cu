@@ -10,6 +10,7 @@
 
 namespace {
 thread_local int g_last_kernel = 0;
+thread_local int g_max_ctas = 0;  // grid cap for the next fused launches (multi-resolution concurrency)
 }  // namespace
 namespace kmd {
 void set_last_kernel(int k) { g_last_kernel = k; }
@@ -123,6 +124,7 @@ kmd_status kmd_decode_filter_fuse_remod(const float* radiance, const float* impo
         return fail(KMD_ERR_ALIAS, "out overlaps an input");
     kmd::FusedParams p{};
     p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out; p.albedo = albedo;
+    p.max_ctas = g_max_ctas;
     p.N = N; p.W = W; p.H = H;
     p.row_base = 0; p.buf_rows = H; p.out_y0 = 0; p.out_rows = H;
     return run_fused(p, cfg, (cudaStream_t)stream);
@@ -421,6 +423,25 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
 
 // ---------------------------------------------------------------------------
 // NEXT row 2: multi-resolution reconstruction (Eq. 7)
+struct MrStreams {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int dev = -1;
+};
+thread_local MrStreams g_ms;
+static cudaError_t mr_streams(MrStreams** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (g_ms.dev != dev) {
+        if ((e = cudaStreamCreateWithFlags(&g_ms.aux, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&g_ms.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&g_ms.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+        g_ms.dev = dev;
+    }
+    *out = &g_ms;
+    return cudaSuccess;
+}
 static size_t mr_level_floats(int N, int H, int W, int l) {
     return (size_t)N * 3 * (size_t)(H >> l) * (size_t)(W >> l);
 }
@@ -513,21 +534,50 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
     for (int l = l0; l < L; ++l)
         if ((e = kmd::launch_down2(r[l - 1], r[l], (long long)N * 3, H >> l, W >> l, st)) != cudaSuccess)
             return cuda_fail(e, "downsample launch");
+    if (L == 1) return kmd_decode_filter_fuse(r[0], importance[0], blend ? blend[0] : nullptr, out, N, H, W,
+                                              &cfg->level[0], stream);
+    // The coarse levels (and their Eq. 7 combines) run on an auxiliary stream,
+    // concurrently with level 0, each persistent launch on its share of the SMs
+    // (proportional to its tiles): the small levels no longer run alone.
+    MrStreams* ms = nullptr;
+    if ((e = mr_streams(&ms)) != cudaSuccess) return cuda_fail(e, "multi-resolution streams");
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long t0 = 0, t12 = 0;
     for (int l = 0; l < L; ++l) {
-        float* dst = (L == 1) ? out : f[l];
-        kmd_status s = kmd_decode_filter_fuse(r[l], importance[l], blend ? blend[l] : nullptr, dst, N, H >> l,
-                                              W >> l, &cfg->level[l], stream);
+        const long long t = (long long)N * (((W >> l) + 51) / 52) * (((H >> l) + 26) / 27);
+        (l == 0 ? t0 : t12) += t;
+    }
+    int cap0 = (int)((double)sms * (double)t0 / (double)(t0 + t12) + 0.5);
+    cap0 = cap0 < 1 ? 1 : (cap0 > sms - 1 ? sms - 1 : cap0);
+    if ((e = cudaEventRecord(ms->fork, st)) != cudaSuccess) return cuda_fail(e, "event record");
+    if ((e = cudaStreamWaitEvent(ms->aux, ms->fork, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    struct CapGuard {
+        ~CapGuard() { g_max_ctas = 0; }
+    } guard;
+    g_max_ctas = sms - cap0;
+    for (int l = 1; l < L; ++l) {
+        kmd_status s = kmd_decode_filter_fuse(r[l], importance[l], blend ? blend[l] : nullptr, f[l], N, H >> l,
+                                              W >> l, &cfg->level[l], ms->aux);
         if (s) return s;
     }
-    if (L == 1) return KMD_OK;
     // Eq. 7 from the coarsest level: c_{L-1} = f_{L-1}; c_l = combine(f_l, c_{l+1}, alpha_l)
     const float* coarse = f[L - 1];
-    for (int l = L - 2; l >= 0; --l) {
-        float* dst = (l == 0) ? out : c[l];
-        if ((e = kmd::launch_combine(f[l], coarse, alpha[l], dst, N, H >> l, W >> l, st)) != cudaSuccess)
+    for (int l = L - 2; l >= 1; --l) {
+        if ((e = kmd::launch_combine(f[l], coarse, alpha[l], c[l], N, H >> l, W >> l, ms->aux)) != cudaSuccess)
             return cuda_fail(e, "combine launch");
-        coarse = dst;
+        coarse = c[l];
     }
+    if ((e = cudaEventRecord(ms->join, ms->aux)) != cudaSuccess) return cuda_fail(e, "event record");
+    g_max_ctas = cap0;
+    kmd_status s0 = kmd_decode_filter_fuse(r[0], importance[0], blend ? blend[0] : nullptr, f[0], N, H, W,
+                                           &cfg->level[0], stream);
+    if (s0) return s0;
+    g_max_ctas = 0;
+    if ((e = cudaStreamWaitEvent(st, ms->join, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    if ((e = kmd::launch_combine(f[0], coarse, alpha[0], out, N, H, W, st)) != cudaSuccess)
+        return cuda_fail(e, "combine launch");
     return KMD_OK;
 }
 

@@ -29,6 +29,7 @@ struct FusedParams {
     int blend_is_logits;
     int sizes[KMD_MAX_SIZES];
     int debug;           // development switches (env KMD_DEBUG); 0 in production
+    int max_ctas;        // > 0: cap on the persistent grid (to share the SMs with a concurrent launch)
     // backward pass A (kmd_bwd_tma.cu): dL/dRhat in; per size i the pair
     // (a_i / den_i, G.R_i) out through the stage buffer and tm_out
     const float* grad;   // [N,3,H,W] or nullptr

@@ -803,7 +803,8 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err != cudaSuccess) return err;
     const size_t smem = sizeof(Smem);
-    const int grid = (int)(n_tiles < sms ? n_tiles : sms);
+    const int cap = p.max_ctas > 0 && p.max_ctas < sms ? p.max_ctas : sms;
+    const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     auto launch = [&](auto kern) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
