@@ -49,3 +49,43 @@ def test_downsample_and_combine_entry_points(oracle_mod, cuda_device):
     o = kmd.combine_resolutions(fine.to(cuda_device), coarse.to(cuda_device), alpha.to(cuda_device))
     torch.cuda.synchronize()
     assert torch.equal(o.cpu(), fine)       # alpha = 0 -> fine, exactly
+
+
+@pytest.mark.parametrize("levels,N,H,W", [(2, 1, 64, 88), (4, 1, 96, 160), (1, 2, 40, 48)])
+def test_mr_other_level_counts(oracle_mod, cuda_device, levels, N, H, W):
+    # 2 levels (no two-level downsample pass), 4 levels (two-level pass + one
+    # more 2x2 pass), 1 level (the plain decoder, no auxiliary stream)
+    sizes = [[3, 5]] * levels
+    mi = gen.make_mr_inputs(N, H, W, sizes_per_level=sizes)
+    out = kmd.mr_decode_filter_fuse(mi.radiance.to(cuda_device), [t.to(cuda_device) for t in mi.importance],
+                                    [t.to(cuda_device) for t in mi.blend],
+                                    [t.to(cuda_device) for t in mi.alpha], sizes)
+    torch.cuda.synchronize()
+    ref = oracle_mod.mr_decode_filter_fuse(mi.radiance.numpy(), [t.numpy() for t in mi.importance],
+                                           [t.numpy() for t in mi.blend], [t.numpy() for t in mi.alpha], sizes)
+    f0 = oracle_mod.decode_filter_fuse(mi.radiance.numpy(), mi.importance[0].numpy(), mi.blend[0].numpy(),
+                                       sizes[0])
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref) / (np.abs(ref) + 2 * np.abs(f0) + 1e-30)
+    assert err.max() <= 1e-5, err.max()
+
+
+def test_mr_inside_cuda_graph_is_bitwise_eager(cuda_device):
+    # the coarse levels fork onto an auxiliary stream and join back: the call
+    # must be capturable and replay to the same bits
+    sizes = [list(s) for s in gen.MR_SIZES]
+    mi = gen.make_mr_inputs(1, 108, 208, device=cuda_device)
+    ws = torch.empty(kmd.mr_workspace_bytes(1, 108, 208, sizes), dtype=torch.uint8, device=cuda_device)
+    eager = kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, sizes, workspace=ws)
+    torch.cuda.synchronize()
+    out = torch.empty_like(eager)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, sizes, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    out.zero_()
+    with torch.cuda.graph(g):
+        kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, sizes, out=out, workspace=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
