@@ -43,3 +43,23 @@ def test_band_matches_oracle(oracle_mod, cuda_device):
     ref = oracle_mod.decode_filter_fuse(inp.radiance.numpy(), inp.importance.numpy(),
                                         inp.blend.numpy(), PAPER, rows=(band.y0, band.y0 + band.rows))
     assert_parity(out.cpu().numpy(), ref, what="band vs oracle")
+
+
+@pytest.mark.parametrize("sizes,W", [([21, 5], 96), ([3, 5, 7], 90)])
+def test_bands_bitwise_other_kernels(cuda_device, sizes, W):
+    # the v1 kernel (k > 13) and the v2 kernel (W % 4 != 0) keep the same
+    # band-invariance: their summation order depends on the global tile grid only
+    H = 160
+    inp = gen.make_inputs(1, H, W, len(sizes), seed=91, device=cuda_device)
+    whole = kmd.decode_filter_fuse(inp.radiance, inp.importance, inp.blend, sizes)
+    kind = kmd.last_kernel()
+    assert kind == ("v1-direct" if max(sizes) > 13 else "v2-ws")
+    for band in B.split_rows(H, 3, sizes):
+        out = kmd.decode_filter_fuse_band(
+            B.slice_band(inp.radiance, band), B.slice_band(inp.importance, band),
+            inp.blend[:, :, band.y0:band.y0 + band.rows].contiguous(), sizes,
+            y0=band.y0, band_rows=band.rows, halo_top=band.halo_top, halo_bot=band.halo_bot,
+            H_global=H)
+        torch.cuda.synchronize()
+        assert kmd.last_kernel() == kind
+        assert torch.equal(out, whole[:, :, band.y0:band.y0 + band.rows]), f"band {band}"
