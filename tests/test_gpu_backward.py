@@ -114,3 +114,20 @@ def test_backward_empty_and_errors(cuda_device):
     with pytest.raises(RuntimeError):
         kmd.decode_filter_fuse_backward(inp.radiance, inp.importance, inp.blend,
                                         torch.zeros_like(inp.radiance), [3, 4])
+
+
+def test_backward_540p_full_frame_tma(oracle_mod, cuda_device):
+    # a quarter of 1080p on the TMA passes: 20 x 19 tiles of 52 x 27 with a
+    # ragged last column, every pixel of both gradients against the fp64 oracle
+    H, W = 540, 960
+    inp = gen.make_inputs(1, H, W, 6, seed=24)
+    G = torch.randn((1, 3, H, W), generator=torch.Generator().manual_seed(9), dtype=torch.float32)
+    dev = cuda_device
+    gI, gB = kmd.decode_filter_fuse_backward(inp.radiance.to(dev), inp.importance.to(dev), inp.blend.to(dev),
+                                             G.to(dev), PAPER)
+    torch.cuda.synchronize()
+    assert kmd.last_kernel() == "bwd-tma"
+    rI, rB = oracle_mod.backward(inp.radiance.numpy(), inp.importance.numpy(), inp.blend.numpy(),
+                                 G.numpy().astype(np.float64), PAPER)
+    _normwise(gI.cpu().numpy(), rI, "540p grad_importance")
+    _normwise(gB.cpu().numpy(), rB, "540p grad_blend")
