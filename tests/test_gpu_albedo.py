@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 PAPER = list(gen.PAPER_SIZES)
 
 
-@pytest.mark.parametrize("H,W,sizes", [(96, 160, PAPER), (37, 45, [3, 5, 7]), (64, 64, [5])])
+@pytest.mark.parametrize("H,W,sizes", [(96, 160, PAPER), (37, 45, [3, 5, 7]), (64, 64, [5]), (540, 960, PAPER)])
 def test_fused_remodulation_matches_oracle(oracle_mod, cuda_device, H, W, sizes):
     inp = gen.make_inputs(1, H, W, len(sizes), seed=11)
     alb = gen.make_albedo(1, H, W)
