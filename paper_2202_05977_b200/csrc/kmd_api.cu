@@ -254,9 +254,13 @@ struct HostBand {
 
 int host_bands(int H, int rmax, HostBand* out) {
     int nb = HOST_MAX_BANDS;
-    while (nb > 1 && H / nb < 2 * rmax + 8) --nb;
+    while (nb > 1 && (int64_t)2 * H / (5 * (nb - 1) + 2) < 2 * rmax + 8) --nb;
+    // the last band is 0.4 of the others: the call ends with that band's kernel
+    // and D2H, which nothing overlaps (the H2D stream is the critical path)
+    const int64_t wsum = 5 * (nb - 1) + 2;
+    auto edge = [&](int b) { return (int)(b == nb ? H : (int64_t)5 * b * H / wsum); };
     for (int b = 0; b < nb; ++b) {
-        const int y0 = (int)((int64_t)b * H / nb), y1 = (int)((int64_t)(b + 1) * H / nb);
+        const int y0 = edge(b), y1 = edge(b + 1);
         out[b].y0 = y0;
         out[b].rows = y1 - y0;
         out[b].top = y0 < rmax ? y0 : rmax;
