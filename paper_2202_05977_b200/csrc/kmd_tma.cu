@@ -53,15 +53,15 @@ static_assert(FW == 64, "two 32-lane field halves per size");
 #define KMD_TH 27
 #endif
 constexpr int TH = KMD_TH;          // output rows per tile
-constexpr int FH = TH + 2 * RMAX;   // 36 field rows in every box
+constexpr int FH = TH + 2 * RMAX;   // 39 field rows in every box
 // Every TMA box starts at column x0-8: the innermost box coordinate must be a
 // multiple of 16 bytes when it is negative (measured on this B200: -6 faults,
 // -8 works), and 68 columns cover x0-6 .. x0+57 (and the 52 output columns).
 constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
 constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
 constexpr int VS = 68;
-constexpr int SEG = 7;              // pixels per fusion thread (segments of 7/6 alternate)
-constexpr int NSEG = 8;             // segments per output row: 52 = 4 x (7 + 6)
+constexpr int SEG = 7;              // pixels per fusion thread (segments of 7 or 6 pixels)
+constexpr int NSEG = 8;             // segments per output row: 52 = 4 x 7 + 4 x 6
 constexpr int NI = TH > 24 ? 3 : 4; // input (importance) ring depth
 constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
 constexpr int NV = 3;               // V ring depth (field -> fusion)
@@ -71,7 +71,7 @@ constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 
 struct InSlot {
-    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+29, cols x0-8 .. x0+59
+    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+32, cols x0-8 .. x0+59
 };
 struct alignas(128) Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
@@ -81,7 +81,7 @@ struct alignas(128) Slot {
 // warp reads at 32 distinct banks
 constexpr int BBW = 56;
 struct BSlot {
-    alignas(128) float B[TH][BBW];     // blend logits of map i, rows y0 .. y0+23, cols x0 .. x0+55
+    alignas(128) float B[TH][BBW];     // blend logits of map i, rows y0 .. y0+26, cols x0 .. x0+55
 };
 struct RadBuf {
     alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
@@ -165,7 +165,7 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
     return c;
 }
 
-// rows of the box (global y0-6 .. y0+29) outside the frame/buffer take the
+// rows of the box (global y0-6 .. y0+32) outside the frame/buffer take the
 // value of the nearest valid row (clamp-to-edge, reading R1)
 __device__ __forceinline__ void fix_rows(float* col, int plane_stride, int nplanes, int top, int bot) {
     for (int pl = 0; pl < nplanes; ++pl) {
