@@ -89,3 +89,24 @@ def test_mr_inside_cuda_graph_is_bitwise_eager(cuda_device):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, eager)
+
+
+def test_mr_error_paths(cuda_device):
+    sizes = [list(s) for s in gen.MR_SIZES]
+    mi = gen.make_mr_inputs(1, 96, 160, device=cuda_device)
+    ws = torch.empty(kmd.mr_workspace_bytes(1, 96, 160, sizes), dtype=torch.uint8, device=cuda_device)
+    # workspace too small
+    with pytest.raises(kmd.KmdError):
+        kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, sizes, workspace=ws[:16])
+    # H not divisible by 2^(levels-1): 3 levels on 94 rows
+    x = gen.make_mr_inputs(1, 96, 160, sizes_per_level=[[3, 5]], device=cuda_device)
+    r94 = x.radiance[:, :, :94].contiguous()
+    imp = [x.importance[0][:, :, :94].contiguous(), torch.zeros((1, 2, 47, 80), device=cuda_device),
+           torch.zeros((1, 2, 23, 40), device=cuda_device)]
+    bl = [t.clone() for t in imp]
+    al = [torch.zeros((1, 1, 94, 160), device=cuda_device), torch.zeros((1, 1, 47, 80), device=cuda_device)]
+    with pytest.raises(kmd.KmdError):
+        kmd.mr_decode_filter_fuse(r94, imp, bl, al, sizes)
+    # an even kernel size in one level
+    with pytest.raises(kmd.KmdError):
+        kmd.mr_decode_filter_fuse(mi.radiance, mi.importance, mi.blend, mi.alpha, [[3, 5], [3, 4], [3, 5]])
