@@ -54,6 +54,8 @@ def parse():
                     help="--mode batch: frames per rank in one launch (BASELINE.json configs[4])")
     ap.add_argument("--albedo", action="store_true",
                     help="NEXT row 1: fuse the albedo remodulation epilogue (out = Rhat * albedo)")
+    ap.add_argument("--bf16", action="store_true",
+                    help="NEXT row 4 alternative: bf16 importance maps and logits (kmd_decode_filter_fuse_bf16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU seconds for the oracle sample")
@@ -248,6 +250,11 @@ def run_kmd(args, rank, world, local):
     kmd.lib()
     # resident inputs: F distinct frames per rank (frame ids rank*F .. rank*F+F-1)
     inp = gen.make_inputs(F, H, W, M, frame_offset=rank * F, device=dev)
+    if args.bf16:
+        # the network's output in bf16; the oracle below sees the same values widened
+        assert not args.albedo, "--bf16 has no albedo epilogue"
+        inp = gen.FrameInputs(inp.radiance, inp.importance.to(torch.bfloat16),
+                              None if inp.blend is None else inp.blend.to(torch.bfloat16))
     outs = torch.empty((F, 3, H, W), device=dev)
     alb = gen.make_albedo(F, H, W, frame_offset=rank * F, device=dev) if args.albedo else None
     views = [(inp.radiance[f:f + 1], inp.importance[f:f + 1],
@@ -313,15 +320,18 @@ def run_kmd(args, rank, world, local):
     value = px_per_step * K / (el_ms_max / 1e3) / 1e6
     bytes_launch = kmd.algorithmic_bytes(1, H, W, sizes, inp.blend is not None) + \
         (12 * H * W if args.albedo else 0)
+    if args.bf16:  # importance and logits at 2 B instead of 4 (48 B/px at M = 6)
+        bytes_launch -= 2 * H * W * (M + (M if inp.blend is not None else 0))
     achieved = bytes_launch / (kern_avg_ms / 1e3) / 1e9
     peak, peak_src = measured_peak_hbm()
     cfg_name = {(1920, 1080): "configs[2]", (1280, 720): "configs[1]"}.get((W, H), "custom size")
     workload = f"{W}x{H} frame, sizes {sizes}, fusion (BASELINE.json {cfg_name})" + \
-        (" + albedo remodulation (NEXT row 1)" if args.albedo else "")
+        (" + albedo remodulation (NEXT row 1)" if args.albedo else "") + \
+        (", bf16 importance/logits (NEXT row 4 alternative)" if args.bf16 else "")
 
     # ---- e2e: through the C ABI with pinned HOST buffers ---------------------
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not args.bf16:  # the host entry point is fp32-only
         hr = inp.radiance[:1].cpu().pin_memory()
         hi = inp.importance[:1].cpu().pin_memory()
         hb = None if inp.blend is None else inp.blend[:1].cpu().pin_memory()
@@ -350,8 +360,8 @@ def run_kmd(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import numpy as np
         import oracle
-        inp_cpu = (inp.radiance[:1].cpu().numpy(), inp.importance[:1].cpu().numpy(),
-                   None if inp.blend is None else inp.blend[:1].cpu().numpy())
+        inp_cpu = (inp.radiance[:1].cpu().numpy(), inp.importance[:1].float().cpu().numpy(),
+                   None if inp.blend is None else inp.blend[:1].float().cpu().numpy())
         rows, _ = calibrate_rows(inp_cpu, sizes, H, args.cpu_seconds)
         y0 = max(0, (H - rows) // 2)
         dt, ref = oracle_rows_time(inp_cpu, sizes, (y0, y0 + rows))

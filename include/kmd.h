@@ -64,7 +64,8 @@ typedef enum {
                            border not KMD_BORDER_CLAMP                                       */
     KMD_ERR_DIM = 3,    /* N < 0, H < 1 or W < 1 (when N > 0); bad band geometry;
                            element count overflows int64                                      */
-    KMD_ERR_ALIGN = 4,  /* reserved (every path accepts any 4-byte aligned pointer)           */
+    KMD_ERR_ALIGN = 4,  /* kmd_decode_filter_fuse_bf16 only: W % 8 != 0 or a buffer not
+                           16-byte aligned (the fp32 entry points accept any 4-byte pointer)  */
     KMD_ERR_ALIAS = 5,  /* out overlaps an input                                              */
     KMD_ERR_CUDA = 6,   /* a CUDA runtime call or launch failed (see kmd_last_error)          */
     KMD_ERR_NCCL = 7    /* reserved for collective helpers                                    */
@@ -94,6 +95,21 @@ typedef void* kmd_stream_t;         /* a cudaStream_t */
 kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance,
                                   const float* blend, float* out, int32_t N, int32_t H,
                                   int32_t W, const kmd_config* cfg, kmd_stream_t stream);
+
+/* Hot path with bf16 importance maps and fusion logits (NEXT row 4's
+ * alternative: the network's output in low precision; the
+ * radiance and the result stay fp32 since the paper's path filters HDR
+ * irradiance).  Same operation as kmd_decode_filter_fuse on the
+ * bf16 values widened exactly to fp32 (R24).
+ *   importance [N,M,H,W] device, bf16 bit patterns (e.g. torch.bfloat16 storage)
+ *   blend      [N,M,H,W] device, bf16; NULL allowed iff M == 1
+ *   radiance, out as kmd_decode_filter_fuse (fp32)
+ * Runs on the TMA kernel only: needs W % 8 == 0 and 16-byte aligned buffers
+ * (else KMD_ERR_ALIGN) and every size <= 13 (else KMD_ERR_CONFIG).
+ * Other errors as kmd_decode_filter_fuse.                                     */
+kmd_status kmd_decode_filter_fuse_bf16(const float* radiance, const uint16_t* importance,
+                                       const uint16_t* blend, float* out, int32_t N, int32_t H,
+                                       int32_t W, const kmd_config* cfg, kmd_stream_t stream);
 
 /* Hot path + remodulation epilogue (NEXT row 1; Fig. 1, 258: "we
  * filter the noisy input irradiance without albedo, and at the last step, we

@@ -73,16 +73,21 @@ kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t str
     static const int dbg = [] { const char* e = getenv("KMD_DEBUG"); return e ? atoi(e) : 0; }();
     p.debug = dbg;
     const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
+    const size_t esz = p.in16 ? 2 : 4;  // bytes per importance / logit element
     const int total = p.N;
     for (int n0 = 0; n0 < total; n0 += 65535) {
         kmd::FusedParams q = p;
         q.N = total - n0 < 65535 ? total - n0 : 65535;
         q.rad = p.rad + (size_t)n0 * 3 * bplane;
-        q.imp = p.imp + (size_t)n0 * p.M * bplane;
-        q.blend = p.blend ? p.blend + (size_t)n0 * p.M * oplane : nullptr;
+        q.imp = (const float*)((const char*)p.imp + (size_t)n0 * p.M * bplane * esz);
+        q.blend = p.blend ? (const float*)((const char*)p.blend + (size_t)n0 * p.M * oplane * esz) : nullptr;
         q.out = p.out + (size_t)n0 * 3 * oplane;
         cudaError_t e;
-        if (kmd::tma_supported(q)) {
+        if (p.in16) {
+            // bf16 inputs: the TMA kernel only (checked by the caller)
+            if (!kmd::tma_supported(q)) return fail(KMD_ERR_ALIGN, "bf16 path needs W %% 8 == 0 and 16-byte aligned buffers");
+            e = kmd::launch_fused_tma(q, stream);
+        } else if (kmd::tma_supported(q)) {
             e = kmd::launch_fused_tma(q, stream);  // records its specialisation
         } else if (kmd::ws_supported(q)) {
             kmd::set_last_kernel(kmd::LK_WS);
@@ -134,6 +139,45 @@ kmd_status kmd_decode_filter_fuse(const float* radiance, const float* importance
                                   const float* blend, float* out, int32_t N, int32_t H,
                                   int32_t W, const kmd_config* cfg, kmd_stream_t stream) {
     return kmd_decode_filter_fuse_remod(radiance, importance, blend, nullptr, out, N, H, W, cfg, stream);
+}
+
+kmd_status kmd_decode_filter_fuse_bf16(const float* radiance, const uint16_t* importance,
+                                       const uint16_t* blend, float* out, int32_t N, int32_t H,
+                                       int32_t W, const kmd_config* cfg, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
+    if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
+    if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
+    if (N > 0) {
+        kmd_status s = check_cfg(cfg, H, W);
+        if (s) return s;
+    }
+    if (N == 0) return KMD_OK;
+    if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
+    if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (W % 8 != 0) return fail(KMD_ERR_ALIGN, "bf16 path needs W %% 8 == 0 (W=%d)", W);
+    const uintptr_t a = (uintptr_t)radiance | (uintptr_t)importance | (uintptr_t)out |
+                        (uintptr_t)(cfg->num_sizes > 1 ? blend : nullptr);
+    if (a & 15) return fail(KMD_ERR_ALIGN, "bf16 path needs 16-byte aligned buffers");
+    const size_t px = (size_t)H * W;
+    const size_t M = (size_t)cfg->num_sizes;
+    if (overlaps(out, 3 * N * px * 4, radiance, 3 * N * px * 4) ||
+        overlaps(out, 3 * N * px * 4, importance, M * N * px * 2) ||
+        (M > 1 && overlaps(out, 3 * N * px * 4, blend, M * N * px * 2)))
+        return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    for (int k = 0; k < cfg->num_sizes; ++k)
+        if ((cfg->sizes[k] - 1) / 2 > 6)
+            return fail(KMD_ERR_CONFIG, "bf16 path supports sizes <= 13 (sizes[%d]=%d)", k, cfg->sizes[k]);
+    kmd::FusedParams p{};
+    p.rad = radiance;
+    p.imp = reinterpret_cast<const float*>(importance);
+    p.blend = reinterpret_cast<const float*>(blend);
+    p.out = out;
+    p.in16 = 1;
+    p.max_ctas = g_max_ctas;
+    p.N = N; p.W = W; p.H = H;
+    p.row_base = 0; p.buf_rows = H; p.out_y0 = 0; p.out_rows = H;
+    return run_fused(p, cfg, (cudaStream_t)stream);
 }
 
 kmd_status kmd_demodulate(const float* radiance, const float* albedo, float eps, float* irradiance,

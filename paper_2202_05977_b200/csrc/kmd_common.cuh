@@ -33,6 +33,8 @@ struct FusedParams {
     // backward pass A (kmd_bwd_tma.cu): dL/dRhat in; per size i the pair
     // (a_i / den_i, G.R_i) out through the stage buffer and tm_out
     const float* grad;   // [N,3,H,W] or nullptr
+    // imp / blend hold bf16 bits (kmd_decode_filter_fuse_bf16; TMA kernel only)
+    int in16;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }

@@ -51,7 +51,7 @@ cudaError_t launch_temporal(const float* cur_rad, const float* prev_rad, const f
 
 // kernel variant of the last fused launch on this host thread (kmd_last_kernel)
 enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_BWD_TILE = 10, LK_BWD_TMA = 11, LK_TMA_SPEC = 100,
-                  LK_TMA_SPEC_ALB = 150 };
+                  LK_TMA_SPEC_ALB = 150, LK_TMA_BF16 = 200 };
 void set_last_kernel(int k);
 
 }  // namespace kmd

@@ -70,33 +70,62 @@ constexpr int NFUSE = (TH * NSEG + 31) / 32;  // fusion warps (one thread per (r
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 
-struct InSlot {
-    alignas(128) float I[FH][BW];      // importance map i, rows y0-6 .. y0+32, cols x0-8 .. x0+59
+// Importance maps and fusion logits arrive as fp32, or as bf16 (NEXT row 4's
+// alternative: the network's low-precision output) -- IN16 below.  A bf16 row
+// of the importance box is 72 elements (144 bytes: TMA rows are multiples of
+// 16 bytes); the logit box stays 56 wide (112 bytes).
+template <bool IN16>
+struct InElem {
+    using T = float;
+    static constexpr int IW = BW;
+};
+template <>
+struct InElem<true> {
+    using T = unsigned short;  // bf16 bits
+    static constexpr int IW = 72;
+};
+__device__ __forceinline__ float ld_in(const float* q) { return *q; }
+__device__ __forceinline__ float ld_in(const unsigned short* q) { return __uint_as_float((unsigned)*q << 16); }
+// A TMA tile load faults (illegal instruction, measured on this B200) unless
+// its first element is 16-byte aligned in global memory.  Tile origins x0 are
+// multiples of 52 = 4 mod 8: fp32 boxes (x0 - 8, x0) are aligned, bf16 boxes
+// start xalign = x0 mod 8 (0 or 4) elements earlier and are indexed that much
+// further in (the 72 / 56 element boxes still cover the tile + halo).
+template <bool IN16>
+__device__ __forceinline__ int xalign(int x0) { return IN16 ? (x0 & 7) : 0; }
+
+template <bool IN16>
+struct InSlotT {
+    alignas(128) typename InElem<IN16>::T I[FH][InElem<IN16>::IW];  // importance map i, rows y0-6 .. y0+32, cols x0-8 ..
 };
 struct alignas(128) Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
 };
 // blend box: the 52 output columns plus 4 of padding, starting at x0 (no
-// halo); the 56-float row stride puts the 4 rows x 8 segment starts a fusion
-// warp reads at 32 distinct banks
+// halo); the 56-element row stride puts the 4 rows x 8 segment starts a fusion
+// warp reads at 32 distinct banks (fp32)
 constexpr int BBW = 56;
-struct BSlot {
-    alignas(128) float B[TH][BBW];     // blend logits of map i, rows y0 .. y0+26, cols x0 .. x0+55
+template <bool IN16>
+struct BSlotT {
+    alignas(128) typename InElem<IN16>::T B[TH][BBW];  // blend logits of map i, rows y0 .. y0+26, cols x0 .. x0+55
 };
 struct RadBuf {
     alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
 };
-struct Smem {
+template <bool IN16>
+struct SmemT {
     RadBuf rad[2];
-    InSlot in[NI];
+    InSlotT<IN16> in[NI];
     Slot slot[NV];
-    BSlot bl[NB];
+    BSlotT<IN16> bl[NB];
     float stage[3][TH][TW];
     unsigned long long rad_full[2], rad_empty[2], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV], b_full[NB],
         b_empty[NB];
 };
-static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlot) % 128 == 0 &&
-                  sizeof(BSlot) % 128 == 0,
+using Smem = SmemT<false>;
+static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlotT<false>) % 128 == 0 &&
+                  sizeof(BSlotT<false>) % 128 == 0 && sizeof(InSlotT<true>) % 128 == 0 &&
+                  sizeof(BSlotT<true>) % 128 == 0,
               "TMA destinations 128-B aligned");
 
 // ---- optional timing instrumentation (build with -DKMD_INSTR; off in production)
@@ -167,30 +196,34 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
 
 // rows of the box (global y0-6 .. y0+32) outside the frame/buffer take the
 // value of the nearest valid row (clamp-to-edge, reading R1)
-__device__ __forceinline__ void fix_rows(float* col, int plane_stride, int nplanes, int top, int bot) {
+template <int STRIDE = BW, class T>
+__device__ __forceinline__ void fix_rows(T* col, int plane_stride, int nplanes, int top, int bot) {
     for (int pl = 0; pl < nplanes; ++pl) {
-        float* c = col + pl * plane_stride;
+        T* c = col + pl * plane_stride;
         if (top > 0) {
-            const float v = c[top * BW];
-            for (int r = 0; r < top; ++r) c[r * BW] = v;
+            const T v = c[top * STRIDE];
+            for (int r = 0; r < top; ++r) c[r * STRIDE] = v;
         }
         if (bot < FH) {
-            const float v = c[(bot - 1) * BW];
-            for (int r = bot; r < FH; ++r) c[r * BW] = v;
+            const T v = c[(bot - 1) * STRIDE];
+            for (int r = bot; r < FH; ++r) c[r * STRIDE] = v;
         }
     }
 }
 
 // ------------------------------------------------------------ field warps
-template <int R>
-__device__ __forceinline__ void field_job(Smem& sm, const InSlot& in, Slot& sl, int rb, int h, int cc) {
+// cc: the thread's field column in the radiance box; ci: the same column in
+// the importance box (they differ by the bf16 box alignment shift, see xa)
+template <int R, class SM, class IS>
+__device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci) {
+    constexpr int IW = sizeof(in.I[0]) / sizeof(in.I[0][0]);
     const int c = h * 32 + (threadIdx.x & 31);
-    const float* Ib = &in.I[RMAX - R][cc];
+    const auto* Ib = &in.I[RMAX - R][ci];
     const float* Rb = &sm.rad[rb].v[0][RMAX - R][cc];
     float4* Vc = &sl.V[0][c];
     gw_line_field<R, TH>(
         [&](int f) {
-            const float v = Ib[f * BW];
+            const float v = ld_in(Ib + f * IW);
             const float r = Rb[f * BW], g = Rb[FH * BW + f * BW], b = Rb[2 * FH * BW + f * BW];
             const float e = exp_acc(v);  // once per field pixel (Eq. 3's shared weight)
             const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(g, b));  // pairs (e, er), (eg, eb)
@@ -238,10 +271,10 @@ __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alph
     st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
 }
 
-template <int MODE>
-__device__ __forceinline__ void fuse_seg(Acc& st, const float* Br, const float4 (&o)[SEG]) {
+template <int MODE, class T>
+__device__ __forceinline__ void fuse_seg(Acc& st, const T* Br, const float4 (&o)[SEG]) {
 #pragma unroll
-    for (int j = 0; j < SEG; ++j) fuse_px<MODE>(st, j, Br[j], o[j]);
+    for (int j = 0; j < SEG; ++j) fuse_px<MODE>(st, j, ld_in(Br + j), o[j]);
 }
 
 // Horizontal box sums of one size for the thread's 13 pixels (templated on
@@ -253,9 +286,9 @@ __device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)
     gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
 }
 
-template <int SMODE>
-__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, const BSlot& bs, Acc& st, int ty,
-                                         int xs, int R) {
+template <int SMODE, class BS>
+__device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, const BS& bs, Acc& st, int ty,
+                                         int xs, int xb, int R) {
     float4 o[SEG];
     switch (R) {
         case 0: hbox<0>(sl, ty, xs, o); break;
@@ -266,7 +299,7 @@ __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, c
         case 5: hbox<5>(sl, ty, xs, o); break;
         default: hbox<6>(sl, ty, xs, o); break;
     }
-    const float* Br = &bs.B[ty][xs];
+    const auto* Br = &bs.B[ty][xb];
     if constexpr (SMODE >= 0) {
         fuse_seg<SMODE>(st, Br, o);  // mode fixed by the kernel's specialisation
     } else {
@@ -281,26 +314,30 @@ __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, c
 __device__ __noinline__ float3 exact_pixel(const FusedParams& p, int n, int x, int y) {
     const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
     const float* rp = p.rad + (size_t)n * 3 * bplane;
+    // element q of an importance / logit array (fp32, or bf16 bits when in16)
+    auto ld = [&](const float* a, size_t q) {
+        return p.in16 ? ld_in(reinterpret_cast<const unsigned short*>(a) + q) : a[q];
+    };
     float mb = -INFINITY;
     if (p.M > 1 && p.blend_is_logits)
         for (int i = 0; i < p.M; ++i)
-            mb = fmaxf(mb, p.blend[((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x]);
+            mb = fmaxf(mb, ld(p.blend, ((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x));
     float S = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f;
     for (int i = 0; i < p.M; ++i) {
         const int R = (p.sizes[i] - 1) / 2;
-        const float* Ii = p.imp + ((size_t)n * p.M + i) * bplane;
+        const size_t Ii = ((size_t)n * p.M + i) * bplane;
         auto off = [&](int dy, int dx) {
             const int gy = clampi(clampi(y + dy, 0, p.H - 1) - p.row_base, 0, p.buf_rows - 1);
             return (size_t)gy * p.W + clampi(x + dx, 0, p.W - 1);
         };
         float m = -INFINITY;
         for (int dy = -R; dy <= R; ++dy)
-            for (int dx = -R; dx <= R; ++dx) m = fmaxf(m, Ii[off(dy, dx)]);
+            for (int dx = -R; dx <= R; ++dx) m = fmaxf(m, ld(p.imp, Ii + off(dy, dx)));
         float den = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
         for (int dy = -R; dy <= R; ++dy)
             for (int dx = -R; dx <= R; ++dx) {
                 const size_t q = off(dy, dx);
-                const float e = expf(Ii[q] - m);
+                const float e = expf(ld(p.imp, Ii + q) - m);
                 den += e;
                 n0 = fmaf(e, rp[q], n0);
                 n1 = fmaf(e, rp[bplane + q], n1);
@@ -308,7 +345,7 @@ __device__ __noinline__ float3 exact_pixel(const FusedParams& p, int n, int x, i
             }
         float a = 1.f;
         if (p.M > 1) {
-            const float b = p.blend[((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x];
+            const float b = ld(p.blend, ((size_t)n * p.M + i) * oplane + (size_t)(y - p.out_y0) * p.W + x);
             a = p.blend_is_logits ? expf(b - mb) : b;
         }
         S += a;
@@ -335,6 +372,13 @@ struct Runtime {
     static constexpr int M = 0;
     static constexpr int MODE = -1;
     static constexpr bool ALB = true;
+    static constexpr bool IN16 = false;
+};
+struct Runtime16 {  // bf16 importance / logits, any M (NEXT row 4's alternative)
+    static constexpr int M = 0;
+    static constexpr int MODE = -1;
+    static constexpr bool ALB = true;
+    static constexpr bool IN16 = true;
 };
 // backward pass A (NEXT row 3): the forward's tiles and box sums, with the
 // fusion epilogue replaced by the per-size gradient field h_i (runtime M)
@@ -342,12 +386,14 @@ struct SpecBwdH {
     static constexpr int M = 0;
     static constexpr int MODE = FUSE_BWD_H;
     static constexpr bool ALB = false;
+    static constexpr bool IN16 = false;
 };
-template <int MODE_, bool ALB_, int M_>
+template <int MODE_, bool ALB_, int M_, bool IN16_ = false>
 struct Spec {
     static constexpr int MODE = MODE_;  // FUSE_SOFTMAX (blend logits)
     static constexpr bool ALB = ALB_;   // albedo epilogue (NEXT row 1)
     static constexpr int M = M_;
+    static constexpr bool IN16 = IN16_;  // bf16 importance / logits
 };
 
 // --------------------------------------------------------------------- kernel
@@ -357,7 +403,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                      const __grid_constant__ CUtensorMap tm_imp, const __grid_constant__ CUtensorMap tm_blend,
                      const __grid_constant__ CUtensorMap tm_out, int tiles_x, int tiles_y, int n_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    using SmemK = SmemT<SP::IN16>;
+    SmemK& sm = *reinterpret_cast<SmemK*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = SP::M > 0 ? SP::M : p.M;
     const bool has_blend = p.blend != nullptr && !(p.debug & 16);
@@ -397,7 +444,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
-            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * BW * 4, B_BYTES = TH * BBW * 4;
+            constexpr unsigned ESZ = SP::IN16 ? 2 : 4;
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * InElem<SP::IN16>::IW * ESZ,
+                               B_BYTES = TH * BBW * ESZ;
             // In-order, blocking issue of every (tile, size) step: radiance
             // (per tile), importance and blend logits.  Deadlock-free: each wait
             // is on a slot released by a step whose inputs were issued earlier
@@ -421,15 +470,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         mbar_arrive(&sm.in_full[s]);
                     } else {
                         mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES);
-                        tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF, tc.y0 - RMAX - p.row_base,
-                                    tc.n * M + i, &sm.in_full[s]);
+                        tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF - xalign<SP::IN16>(tc.x0),
+                                    tc.y0 - RMAX - p.row_base, tc.n * M + i, &sm.in_full[s]);
                     }
                     if (has_blend) {
                         const int sb = seq % NB;
                         IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
                         mbar_arrive_expect_tx(&sm.b_full[sb], B_BYTES);
-                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0, tc.y0 - p.out_y0, tc.n * M + i,
-                                    &sm.b_full[sb]);
+                        tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0 - xalign<SP::IN16>(tc.x0),
+                                    tc.y0 - p.out_y0, tc.n * M + i, &sm.b_full[sb]);
                     }
                 }
             }
@@ -451,16 +500,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int seq = tl * M + i, si = seq % NI, sv = seq % NV;
                 const int c = h * 32 + lane;
                 const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
+                const int ci = cc + xalign<SP::IN16>(tc.x0);
                 Slot& sl = sm.slot[sv];
-                InSlot& in = sm.in[si];
+                auto& in = sm.in[si];
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
                 IWAIT(4, mbar_wait(&sm.in_full[si], (seq / NI) & 1));
                 if (border_rows && !(p.debug & 4)) {
-                    fix_rows(&in.I[0][cc], FH * BW, 1, top, bot);
+                    fix_rows<InElem<SP::IN16>::IW>(&in.I[0][ci], FH * BW, 1, top, bot);
                     fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
                     fence_proxy_async();  // generic writes before the next TMA overwrite
                 }
-                if (!(p.debug & 32)) body(in, sl, cc);
+                if (!(p.debug & 32)) body(in, sl, cc, ci);
                 // one arrive per warp: __syncwarp orders every lane's shared
                 // memory accesses before the elected lane's release-arrive
                 __syncwarp();
@@ -473,15 +523,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
                 for (int jl = fw; jl < 2 * M; jl += NFIELD) {
                     const int i = jl >> 1, h = jl & 1;
-                    job(i, h, [&](const InSlot& in, Slot& sl, int cc) {
+                    job(i, h, [&](const auto& in, Slot& sl, int cc, int ci) {
                         switch ((rpack >> (4 * i)) & 15) {
-                            case 0: field_job<0>(sm, in, sl, rb, h, cc); break;
-                            case 1: field_job<1>(sm, in, sl, rb, h, cc); break;
-                            case 2: field_job<2>(sm, in, sl, rb, h, cc); break;
-                            case 3: field_job<3>(sm, in, sl, rb, h, cc); break;
-                            case 4: field_job<4>(sm, in, sl, rb, h, cc); break;
-                            case 5: field_job<5>(sm, in, sl, rb, h, cc); break;
-                            default: field_job<6>(sm, in, sl, rb, h, cc); break;
+                            case 0: field_job<0>(sm, in, sl, rb, h, cc, ci); break;
+                            case 1: field_job<1>(sm, in, sl, rb, h, cc, ci); break;
+                            case 2: field_job<2>(sm, in, sl, rb, h, cc, ci); break;
+                            case 3: field_job<3>(sm, in, sl, rb, h, cc, ci); break;
+                            case 4: field_job<4>(sm, in, sl, rb, h, cc, ci); break;
+                            case 5: field_job<5>(sm, in, sl, rb, h, cc, ci); break;
+                            default: field_job<6>(sm, in, sl, rb, h, cc, ci); break;
                         }
                     });
                 }
@@ -561,12 +611,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             case 5: hbox<5>(sm.slot[vs], ty, xs, o); break;
                             default: hbox<6>(sm.slot[vs], ty, xs, o); break;
                         }
-                        const float* Br = &sm.bl[bs].B[ty][xs];
+                        const auto* Br = &sm.bl[bs].B[ty][xs];
 #pragma unroll
                         for (int j = 0; j < SEG; ++j) {
                             const float rden = rcp_approx(o[j].x);
                             const float R0 = o[j].y * rden, R1 = o[j].z * rden, R2 = o[j].w * rden;
-                            const float a = M == 1 ? 1.f : (logits ? exp_acc(Br[j] - mb[j]) * is[j] : Br[j]);
+                            const float bj = ld_in(Br + j);
+                            const float a = M == 1 ? 1.f : (logits ? exp_acc(bj - mb[j]) * is[j] : bj);
                             sv[j] = a * rden;
                             dv[j] = fmaf(G[j][0], R0, fmaf(G[j][1], R1, G[j][2] * R2));
                         }
@@ -624,7 +675,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < M; ++i) {
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                if (!(p.debug & 64) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, (rpack >> (4 * i)) & 15);
+                if (!(p.debug & 64) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
+                                                                   (rpack >> (4 * i)) & 15);
                 __syncwarp();
                 if ((c & 31) == 0) {
                     mbar_arrive(&sm.v_empty[vs]);
@@ -719,14 +771,17 @@ EncodeFn get_encode() {
     return fn;
 }
 
-bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long planes, int bw, int bh, int bp) {
+bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long planes, int bw, int bh, int bp,
+              bool bf16 = false) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
+    const cuuint64_t es = bf16 ? 2 : 4;
     const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)planes};
-    const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * 4 * rows};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * es, (cuuint64_t)W * es * rows};
     const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bp};
     const cuuint32_t estr[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+               const_cast<float*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -771,7 +826,7 @@ cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream) {
 }
 
 bool tma_supported(const FusedParams& p) {
-    if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % 4 != 0) return false;
+    if (p.M < 1 || p.M > KMD_MAX_SIZES || p.W % (p.in16 ? 8 : 4) != 0) return false;
     for (int i = 0; i < p.M; ++i)
         if ((p.sizes[i] - 1) / 2 > tma::RMAX) return false;
     const uintptr_t a = (uintptr_t)p.rad | (uintptr_t)p.imp | (uintptr_t)p.out | (uintptr_t)p.blend;  // albedo: LDG
@@ -787,12 +842,13 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
     if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
     CUtensorMap m_rad, m_imp, m_blend, m_out;
+    const bool b16 = p.in16 != 0;
     if (!make_map(&m_rad, p.rad, p.W, p.buf_rows, 3LL * p.N, BW, FH, 3) ||
-        !make_map(&m_imp, p.imp, p.W, p.buf_rows, (long long)p.M * p.N, BW, FH, 1) ||
+        !make_map(&m_imp, p.imp, p.W, p.buf_rows, (long long)p.M * p.N, b16 ? InElem<true>::IW : BW, FH, 1, b16) ||
         !make_map(&m_out, p.out, p.W, p.out_rows, 3LL * p.N, TW, TH, 3))
         return cudaErrorInvalidValue;
     if (p.blend) {
-        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BBW, TH, 1))
+        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BBW, TH, 1, b16))
             return cudaErrorInvalidValue;
     } else {
         m_blend = m_imp;  // never used
@@ -802,7 +858,7 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     if (err != cudaSuccess) return err;
     err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err != cudaSuccess) return err;
-    const size_t smem = sizeof(Smem);
+    const size_t smem = b16 ? sizeof(SmemT<true>) : sizeof(Smem);
     const int cap = p.max_ctas > 0 && p.max_ctas < sms ? p.max_ctas : sms;
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     auto launch = [&](auto kern) {
@@ -815,11 +871,16 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     // the multi-resolution levels' M = 2, the sweep-M configurations), M = 6 with
     // the albedo epilogue, and M = 1 (no fusion)
     const bool softmax = p.blend != nullptr && p.blend_is_logits, alb = p.albedo != nullptr;
+    auto spec = [&](auto kern, int code) {
+        set_last_kernel(code);
+        return launch(kern);
+    };
+    if (b16) {
+        // bf16 importance / logits: the paper's configuration specialised, any other M at run time
+        if (softmax && !alb && p.M == 6) return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6, true>>, LK_TMA_BF16 + 6);
+        return spec(fused_tma_kernel<Runtime16>, LK_TMA_BF16);
+    }
     if (!(p.debug & 2048)) {
-        auto spec = [&](auto kern, int code) {
-            set_last_kernel(code);
-            return launch(kern);
-        };
         if (softmax && !alb) switch (p.M) {
                 case 2: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>, LK_TMA_SPEC + 2);
                 case 3: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 3>>, LK_TMA_SPEC + 3);

@@ -66,7 +66,8 @@ def make_mr_config(sizes_per_level: Sequence[Sequence[int]]) -> kmd_mr_config:
 
 _lib = None
 
-EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
+EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_bf16", "kmd_decode_filter_fuse_remod",
+           "kmd_demodulate",
            "kmd_mr_workspace_bytes", "kmd_mr_decode_filter_fuse", "kmd_downsample2x2",
            "kmd_combine_resolutions", "kmd_backward_workspace_bytes",
            "kmd_decode_filter_fuse_backward", "kmd_temporal_accumulate",
@@ -90,6 +91,7 @@ def lib(build_if_missing: bool = True):
     C = ctypes.POINTER(kmd_config)
     L.kmd_decode_filter_fuse.argtypes = [P, P, P, P, i32, i32, i32, C, P]
     L.kmd_decode_filter_fuse_remod.argtypes = [P, P, P, P, P, i32, i32, i32, C, P]
+    L.kmd_decode_filter_fuse_bf16.argtypes = [P, P, P, P, i32, i32, i32, C, P]
     L.kmd_demodulate.argtypes = [P, P, ctypes.c_float, P, i32, i32, i32, P]
     L.kmd_remodulate.argtypes = [P, P, P, i32, i32, i32, P]
     L.kmd_decode_filter.argtypes = [P, P, P, i32, i32, i32, i32, P]
@@ -120,7 +122,8 @@ def lib(build_if_missing: bool = True):
     L.kmd_version.argtypes = []
     L.kmd_last_kernel.argtypes = []
     L.kmd_last_kernel.restype = ctypes.c_int32
-    for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_remod", "kmd_demodulate",
+    for f in ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_bf16", "kmd_decode_filter_fuse_remod",
+              "kmd_demodulate",
               "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
               "kmd_downsample2x2", "kmd_combine_resolutions", "kmd_decode_filter_fuse_backward",
               "kmd_temporal_accumulate",
@@ -135,11 +138,11 @@ def _check(status: int):
         raise KmdError(status, lib().kmd_last_error().decode())
 
 
-def _dev_f32(name: str, t: torch.Tensor, shape=None) -> int:
+def _dev_f32(name: str, t: torch.Tensor, shape=None, dtype=torch.float32) -> int:
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {str(dtype).replace('torch.', '')}, got {t.dtype}")
     if t.device.type != "cuda":
         raise ValueError(f"{name} must be a CUDA tensor (libkmd has no CPU path)")
     if not t.is_contiguous():
@@ -163,17 +166,25 @@ def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
     """Fused Eq. 3 -> 4 -> 5: radiance [N,3,H,W], importance [N,M,H,W],
     blend [N,M,H,W] (None iff M==1) -> out [N,3,H,W] (fp32, CUDA).  With
     ``albedo`` [N,3,H,W] the result is remodulated in the same pass
-    (out = Rhat * albedo, PAPER.md:181, 258)."""
+    (out = Rhat * albedo).  bfloat16 importance / blend
+    (both, radiance stays fp32) select kmd_decode_filter_fuse_bf16 (W % 8 == 0)."""
     N, C, H, W = radiance.shape
     M = len(sizes)
+    in16 = isinstance(importance, torch.Tensor) and importance.dtype == torch.bfloat16
+    idt = torch.bfloat16 if in16 else torch.float32
     rp = _dev_f32("radiance", radiance, (N, 3, H, W))
-    ip = _dev_f32("importance", importance, (N, M, H, W))
-    bp = None if blend is None else _dev_f32("blend", blend, (N, M, H, W))
+    ip = _dev_f32("importance", importance, (N, M, H, W), idt)
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, H, W), idt)
     if out is None:
         out = torch.empty((N, 3, H, W), device=radiance.device, dtype=torch.float32)
     op = _dev_f32("out", out, (N, 3, H, W))
     cfg = make_config(sizes, blend_is_logits)
-    if albedo is None:
+    if in16:
+        if albedo is not None:
+            raise ValueError("albedo remodulation is not available with bf16 inputs")
+        _check(lib().kmd_decode_filter_fuse_bf16(rp, ip, bp, op, N, H, W, ctypes.byref(cfg),
+                                                 _stream(radiance, stream)))
+    elif albedo is None:
         _check(lib().kmd_decode_filter_fuse(rp, ip, bp, op, N, H, W, ctypes.byref(cfg),
                                             _stream(radiance, stream)))
     else:
@@ -315,8 +326,11 @@ LAST_KERNEL = {0: "none", 1: "v1-direct", 2: "v2-ws", 3: "v3-tma", 10: "bwd-tile
 
 def last_kernel() -> str:
     """Kernel variant of the last fused launch on this thread (diagnostic):
-    v1-direct, v2-ws, v3-tma (runtime M), v3-tma-M<m>[-albedo] (compiled for M)."""
+    v1-direct, v2-ws, v3-tma (runtime M), v3-tma-M<m>[-albedo] (compiled for M),
+    v3-tma-bf16[-M<m>] (bf16 importance / logits)."""
     code = int(lib().kmd_last_kernel())
+    if code >= 200:
+        return f"v3-tma-bf16-M{code - 200}" if code > 200 else "v3-tma-bf16"
     if code >= 150:
         return f"v3-tma-M{code - 150}-albedo"
     if code >= 100:

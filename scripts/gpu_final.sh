@@ -4,7 +4,7 @@ TAG=${1:-final}
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_$TAG.log
-for m in "--albedo" "--mode mr" "--mode band" "--mode bwd" "--mode temporal" "--mode sweep" "--mode batch" "--impl reference --steps 3 --warmup 3"; do
+for m in "--albedo" "--bf16" "--mode mr" "--mode band" "--mode bwd" "--mode temporal" "--mode sweep" "--mode batch" "--impl reference --steps 3 --warmup 3"; do
   n=$(echo $m | tr -d ' -' )
   timeout 600 python bench.py $m 2>&1 | grep '^{' | tail -1 > gpurun_out/bench_${TAG}_$n.json
 done

@@ -10,7 +10,7 @@ for l in open(sys.argv[1]):
         d=json.loads(l); print("BENCH", d["value"], "us", d["kernel_ms"]["avg"]*1e3, "frac", d["roofline"]["frac"])
 PY
 if [ -n "$ALL" ]; then
-for m in "--albedo" "--mode mr" "--mode band" "--mode bwd" "--mode temporal"; do
+for m in "--albedo" "--bf16" "--mode mr" "--mode band" "--mode bwd" "--mode temporal"; do
   timeout 300 python bench.py --steps 400 --warmup 10 --no-cpu-baseline --e2e-steps 0 $m 2>&1 | grep '^{' | python -c "
 import sys,json
 d=json.loads(sys.stdin.read().splitlines()[-1]); print('$m', round(d['value'],1), d['unit'], 'ms/step', round(d['ms_per_step']*1e3,1), 'us')"

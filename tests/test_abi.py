@@ -109,3 +109,24 @@ def test_binding_rejects_cpu_tensors(kmdmod):
     x = torch.zeros(1, 3, 8, 8)
     with pytest.raises(ValueError, match="CUDA"):
         kmdmod.decode_filter_fuse(x, torch.zeros(1, 1, 8, 8), None, [3])
+
+
+def test_bf16_entry_point_errors(L, kmdmod):
+    # kmd_decode_filter_fuse_bf16 (NEXT row 4's alternative): checks precede CUDA
+    f = L.kmd_decode_filter_fuse_bf16
+    cfg = kmdmod.make_config([3, 5])
+    args = (0x1000, 0x100000, 0x200000, 0x40000000)
+    assert f(*args, 1, 64, 60, ctypes.byref(cfg), None) == 4          # W % 8 != 0
+    assert f(0x1004, *args[1:], 1, 64, 64, ctypes.byref(cfg), None) == 4  # misaligned radiance
+    assert f(*args[:2], None, args[3], 1, 64, 64, ctypes.byref(cfg), None) == 1  # M > 1 needs blend
+    assert f(*args[:3], 0x100000 + 16, 1, 64, 64, ctypes.byref(cfg), None) == 5  # out overlaps importance
+    assert f(*args, 1, 64, 64, ctypes.byref(kmdmod.make_config([3, 15])), None) == 2  # k > 13
+    assert f(*args, -1, 64, 64, ctypes.byref(cfg), None) == 3
+    assert f(None, None, None, None, 0, 0, 0, ctypes.byref(cfg), None) == 0  # N == 0: no-op
+
+
+def test_binding_bf16_dtype_checks(kmdmod):
+    import torch
+    x = torch.zeros(1, 3, 8, 8)
+    with pytest.raises(ValueError, match="CUDA"):
+        kmdmod.decode_filter_fuse(x, torch.zeros(1, 1, 8, 8, dtype=torch.bfloat16), None, [3])
