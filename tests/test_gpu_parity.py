@@ -181,3 +181,21 @@ def test_aliasing_rejected_on_device(cuda_device):
     with pytest.raises(kmd.KmdError, match="ALIAS"):
         kmd.decode_filter_fuse(x, torch.zeros((1, 1, 16, 16), device=cuda_device), None, [3],
                                out=x)
+
+
+@pytest.mark.parametrize("N,H,W,sizes", [(1, 61, 108, PAPER), (2, 40, 64, [3, 7, 11])])
+def test_unaligned_buffers(oracle_mod, cuda_device, N, H, W, sizes):
+    # W % 4 == 0 but every buffer starts 4 bytes past a 16-byte boundary: TMA
+    # cannot address it, so the v2 kernel (plain loads) runs
+    inp = gen.make_inputs(N, H, W, len(sizes), seed=2500 + W)
+
+    def shifted(t):
+        flat = torch.empty(t.numel() + 1, device=cuda_device)
+        v = flat[1:].view(t.shape)
+        v.copy_(t.to(cuda_device))
+        return v
+    out = shifted(torch.zeros(N, 3, H, W))
+    kmd.decode_filter_fuse(shifted(inp.radiance), shifted(inp.importance), shifted(inp.blend), sizes, out=out)
+    torch.cuda.synchronize()
+    assert kmd.last_kernel() == "v2-ws"
+    assert_parity(out.cpu().numpy(), _oracle(oracle_mod, inp, sizes), what=f"unaligned {N}x{H}x{W}")
