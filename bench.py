@@ -535,6 +535,7 @@ def run_mr(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": measured_peak_hbm()[0],
                      "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / measured_peak_hbm()[0],
                      "algorithmic_bytes_per_launch": algo,
+                     "traffic": recorded_traffic(f"{W}x{H} multi-resolution reconstruction (NEXT row 2)"),
                      "note": "6 launches per step (one 2-level downsample, 3 fused, 2 combine); algorithmic = inputs + output once"},
         "clocks": clk.summary(), "gpu_launches": steps * 6,
         "paper_context": "Ours MR reconstruction 0.85 ms at 1280x720 on an RTX 2080 Ti (PAPER.md:435)"}),
@@ -598,6 +599,7 @@ def run_bwd(args, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": algo / (ms / 1e3) / 1e9 / peak,
                      "algorithmic_bytes_per_launch": algo,
+                     "traffic": recorded_traffic(f"{W}x{H} backward of the fused decoder (NEXT row 3)"),
                      "kernel": kmd.last_kernel(),
                      "note": f"{kmd.backward_launches_per_call(M)} launches per step (pass A: s_i = a_i / den_i and d_i = G.R_i, pass B: "
                              "transposed box + dL/dI, pass C: dL/dB); algorithmic = inputs + outputs once, the "
@@ -662,7 +664,8 @@ def run_temporal(args, rank, world, local):
                                         "history_kept": round(mask_rate, 3),
                                         "l2": f"{F} resident frames of 94 B/px rotate ({F * H * W * 94 / 1e6:.0f} MB > 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": algo / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo},
+                     "frac": algo / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo,
+                     "traffic": recorded_traffic(f"{W}x{H} reproject + consistency + EMA (NEXT row 4)")},
         "clocks": clk.summary(), "gpu_launches": steps}), flush=True)
 
 
