@@ -61,7 +61,8 @@ __device__ __forceinline__ void fill_field(float4* dst, int base, F1& f1) {
 // keeps the hot loop closer to the I-cache).  Measured and not kept: field
 // values in pairs with packed FP32 exp (2% slower); folding the first block
 // into the loop as well (another 7% less code, 5% slower); unrolling the
-// block loop by 2 to drop the loop-carried MOVs (1-10% slower: code size).
+// block loop by 2 for every radius to drop the loop-carried MOVs (1-10%
+// slower: code size; kept for R = 1 only, below).
 template <int R, int N, class F1, class E>
 __device__ __forceinline__ void gw_line_field(F1&& f1, E&& emit) {
     constexpr int K = 2 * R + 1;
@@ -71,8 +72,7 @@ __device__ __forceinline__ void gw_line_field(F1&& f1, E&& emit) {
 #pragma unroll
     for (int t = K - 2; t >= 0; --t) suf[t] = add4(suf[t], suf[t + 1]);
     // blocks 0 .. NBLK-2: every output and every next-block field index is in range
-#pragma unroll 1
-    for (int b = 0; b < NBLK - 1; ++b) {
+    auto block = [&](int b) {
         const int x0 = b * K;
         emit(x0, suf[0]);
         float4 raw[K];
@@ -87,6 +87,24 @@ __device__ __forceinline__ void gw_line_field(F1&& f1, E&& emit) {
         for (int t = K - 2; t >= 0; --t) raw[t] = add4(raw[t], raw[t + 1]);
 #pragma unroll
         for (int t = 0; t < K; ++t) suf[t] = raw[t];
+    };
+    // The block loop of the smallest radius (k = 3: 3-row blocks, the least
+    // ILP per iteration) is unrolled by 2: measured 0.4-0.6 us faster per
+    // 1080p frame; unrolling R = 2 as well (+0.7 us), R <= 3 (+3 us) or by 3-4
+    // (no gain) was not.  Same operations in the same order: results unchanged.
+#ifndef KMD_GW_UNROLL_RMAX
+#define KMD_GW_UNROLL_RMAX 1
+#endif
+#ifndef KMD_GW_UNROLL_N
+#define KMD_GW_UNROLL_N 2
+#endif
+    constexpr int kUnroll = KMD_GW_UNROLL_N;
+    if constexpr (R <= KMD_GW_UNROLL_RMAX) {
+#pragma unroll kUnroll
+        for (int b = 0; b < NBLK - 1; ++b) block(b);
+    } else {
+#pragma unroll 1
+        for (int b = 0; b < NBLK - 1; ++b) block(b);
     }
     // last block: outputs X0 .. N-1
     constexpr int X0 = (NBLK - 1) * K;
