@@ -601,9 +601,9 @@ def run_bwd(args, rank, world, local):
                      "algorithmic_bytes_per_launch": algo,
                      "traffic": recorded_traffic(f"{W}x{H} backward of the fused decoder (NEXT row 3)"),
                      "kernel": kmd.last_kernel(),
-                     "note": f"{kmd.backward_launches_per_call(M)} launches per step (pass A: s_i = a_i / den_i and d_i = G.R_i, pass B: "
+                     "note": f"{kmd.backward_launches_per_call(M)} launches per step (log-sum-exp of the logits, pass A: s_i = a_i / den_i and d_i = G.R_i, pass B: "
                              "transposed box + dL/dI, pass C: dL/dB); algorithmic = inputs + outputs once, the "
-                             "(s_i, d_i) workspace (8 M B/px written and read) is not counted"},
+                             "(s_i, d_i, L) workspace (8 M + 4 B/px written and read) is not counted"},
         "clocks": clk.summary(), "gpu_launches": steps * kmd.backward_launches_per_call(M)}),
         flush=True)
 

@@ -317,6 +317,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// Log-sum-exp of the M logits per pixel, L = m + log sum_i exp(B_i - m),
+// m = max_i B_i, for pass A's softmax weights a_i = exp(B_i - L) (Eq. 5,
+// PAPER.md:251).  Four pixels per thread (plane % 4 == 0 on the TMA path).
+__global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ blend, float* __restrict__ lse, int M,
+                                                  int plane) {
+    const int nq = plane / 4;
+    const size_t f0 = (size_t)blockIdx.y * M * plane;
+    for (int t = blockIdx.x * 256 + threadIdx.x; t < nq; t += gridDim.x * 256) {
+        float4 b[KMD_MAX_SIZES];
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i) {
+            if (i >= M) break;
+            b[i] = __ldg(reinterpret_cast<const float4*>(blend + f0 + (size_t)i * plane) + t);
+        }
+        float4 m = b[0];
+#pragma unroll
+        for (int i = 1; i < KMD_MAX_SIZES; ++i) {
+            if (i >= M) break;
+            m = make_float4(fmaxf(m.x, b[i].x), fmaxf(m.y, b[i].y), fmaxf(m.z, b[i].z), fmaxf(m.w, b[i].w));
+        }
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < KMD_MAX_SIZES; ++i) {
+            if (i >= M) break;
+            s.x += expf(b[i].x - m.x);
+            s.y += expf(b[i].y - m.y);
+            s.z += expf(b[i].z - m.z);
+            s.w += expf(b[i].w - m.w);
+        }
+        reinterpret_cast<float4*>(lse + (size_t)blockIdx.y * plane)[t] =
+            make_float4(m.x + logf(s.x), m.y + logf(s.y), m.z + logf(s.z), m.w + logf(s.w));
+    }
+}
+
 // pass C: dL/dB_i = a_i (G.R_i - sum_j a_j G.R_j), a = softmax(B) (logits).
 // One thread per 4 consecutive pixels of a frame (float4 when plane % 4 == 0);
 // blockIdx.y = frame, so no 64-bit division per element.
@@ -417,7 +451,10 @@ bool bwd_tma_supported(int H, int W, int M, const int* sizes, const void* a, con
 }
 
 // (s_i, d_i) per pixel and size: [N*M][2][H][W] floats
-size_t bwd_tma_workspace_bytes(int N, int H, int W, int M) { return (size_t)N * M * H * W * 2 * sizeof(float); }
+// (s_i, d_i) planes [N*M][2][H][W], then the log-sum-exp plane [N][H][W]
+size_t bwd_tma_workspace_bytes(int N, int H, int W, int M) {
+    return ((size_t)N * M * H * W * 2 + (size_t)N * H * W) * sizeof(float);
+}
 
 cudaError_t launch_backward_tma(const float* rad, const float* imp, const float* blend, const float* G, float* gI,
                                 float* gB, int N, int H, int W, int M, const int* sizes, int logits, void* ws,
@@ -448,6 +485,19 @@ cudaError_t launch_backward_tma(const float* rad, const float* imp, const float*
     }
     p.rmax = rmax;
     p.grad = G;
+    if (M > 1 && logits) {
+        // ---- log-sum-exp of the logits per pixel (pass A's softmax weights)
+        float* lse = sd + (size_t)N * M * H * W * 2;
+        const int plane = H * W, nq = plane / 4;
+        int dev0 = 0, sms0 = 148;
+        cudaGetDevice(&dev0);
+        cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+        const int gx = (nq + 255) / 256 < sms0 * 8 ? (nq + 255) / 256 : sms0 * 8;
+        lse_kernel<<<dim3(gx, N), 256, 0, st>>>(blend, lse, M, plane);
+        cudaError_t e0 = cudaGetLastError();
+        if (e0 != cudaSuccess) return e0;
+        p.lse = lse;
+    }
     static const int dbg = [] { const char* s = getenv("KMD_DEBUG"); return s ? atoi(s) : 0; }();
     p.debug = dbg;
     cudaError_t e = launch_bwd_h_tma(p, sd, st);

@@ -33,6 +33,7 @@ struct FusedParams {
     // backward pass A (kmd_bwd_tma.cu): dL/dRhat in; per size i the pair
     // (a_i / den_i, G.R_i) out through the stage buffer and tm_out
     const float* grad;   // [N,3,H,W] or nullptr
+    const float* lse;    // [N,H,W] log sum_i exp(B_i) per pixel, or nullptr (pass A's softmax)
     // imp / blend hold bf16 bits (kmd_decode_filter_fuse_bf16; TMA kernel only)
     int in16;
 };

@@ -574,7 +574,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mb[j] = 0.f;
                     is[j] = 1.f;
                 }
-                if (logits) {
+                if (logits && p.lse) {
+                    // a_i = exp(B_i - L) with L = log sum_i exp(B_i) from the
+                    // log-sum-exp pass: one load per pixel instead of M (the M
+                    // strided logit loads per pixel cost 26 us of the step)
+                    const float* lp = p.lse + (size_t)tc.n * plane + (size_t)gyc * p.W;
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) mb[j] = __ldg(lp + min(tc.x0 + xs + j, p.W - 1));
+                } else if (logits) {
                     // softmax shift and normaliser of the logits (Eq. 5): every load
                     // issued before any is used (a dependent chain per pixel would
                     // expose one L2 latency per logit)

@@ -448,13 +448,14 @@ def decode_filter_fuse_backward(radiance: torch.Tensor, importance: torch.Tensor
     return grad_importance, grad_blend
 
 
-def backward_launches_per_call(M: int, path: Optional[str] = None) -> int:
+def backward_launches_per_call(M: int, path: Optional[str] = None, blend_is_logits: bool = True) -> int:
     """Kernel launches of one decode_filter_fuse_backward call: the TMA path
-    ("bwd-tma") runs pass A, pass B and pass C (or a memset when M == 1); the
-    one-launch tiled fallback ("bwd-tile") adds a memset when M == 1."""
+    ("bwd-tma") runs the log-sum-exp pass (M > 1 with logits), pass A, pass B
+    and pass C (or a memset when M == 1); the one-launch tiled fallback
+    ("bwd-tile") adds a memset when M == 1."""
     path = path or last_kernel()
     if path == "bwd-tma":
-        return 3
+        return 4 if M > 1 and blend_is_logits else 3
     return 1 if M > 1 else 2
 
 
