@@ -656,19 +656,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 continue;
 
             }
-            // albedo of this thread's pixels, loaded now so the latency hides
-            // behind the M sizes (remodulation epilogue)
-            float alb[SEG][3];
-            if (SP::ALB && p.albedo && active) {
+            // The tile's albedo (remodulation epilogue),
+            // loaded now so the latency hides behind the M sizes: float4s along
+            // the rows, thread c owning stage float4s c, c + 224, ... (loads
+            // of each thread's own 7-pixel segments would touch every 32-byte
+            // sector ~7 times); applied to the staged tile before its store.
+            constexpr int ALBQ = 3 * TH * (TW / 4), ALBN = (ALBQ + NFUSE * 32 - 1) / (NFUSE * 32);
+            float4 albv[ALBN];
+            if (SP::ALB && p.albedo) {
                 const size_t op = (size_t)p.out_rows * p.W;
-                const int gyc = clampi(tc.y0 + ty - p.out_y0, 0, p.out_rows - 1);
-                const float* ab = p.albedo + (size_t)tc.n * 3 * op + (size_t)gyc * p.W;
 #pragma unroll
-                for (int j = 0; j < SEG; ++j) {
-                    const int gxc = min(tc.x0 + xs + j, p.W - 1);
-                    alb[j][0] = __ldg(ab + gxc);
-                    alb[j][1] = __ldg(ab + op + gxc);
-                    alb[j][2] = __ldg(ab + 2 * op + gxc);
+                for (int k = 0; k < ALBN; ++k) {
+                    const int idx = min(c + k * NFUSE * 32, ALBQ - 1);
+                    const int ch = idx / (TH * (TW / 4)), rem = idx - ch * (TH * (TW / 4));
+                    const int r = rem / (TW / 4), q = rem - r * (TW / 4);
+                    const int gyc = clampi(tc.y0 + r - p.out_y0, 0, p.out_rows - 1);
+                    const int gxc = min(tc.x0 + 4 * q, p.W - 4);  // W % 4 == 0: whole float4s
+                    albv[k] = __ldg(reinterpret_cast<const float4*>(p.albedo + ((size_t)tc.n * 3 + ch) * op +
+                                                                    (size_t)gyc * p.W + gxc));
                 }
             }
             Acc st;
@@ -710,11 +715,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 bad |= b ? (1u << j) : 0u;
                 if (j < len && active) {
                     float r0 = o0, r1 = o1, r2 = o2;
-                    if (SP::ALB && p.albedo) {
-                        r0 *= alb[j][0];
-                        r1 *= alb[j][1];
-                        r2 *= alb[j][2];
-                    }
                     sm.stage[0][ty][xs + j] = r0;
                     sm.stage[1][ty][xs + j] = r1;
                     sm.stage[2][ty][xs + j] = r2;
@@ -726,10 +726,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
                         float3 e = exact_pixel(p, tc.n, gx, gy);
-                        remodulate(p, tc.n, gy, gx, e.x, e.y, e.z);
                         sm.stage[0][ty][xs + j] = e.x;
                         sm.stage[1][ty][xs + j] = e.y;
                         sm.stage[2][ty][xs + j] = e.z;
+                    }
+                }
+            }
+            if (SP::ALB && p.albedo) {
+                fuse_bar();  // the whole tile is staged
+#pragma unroll
+                for (int k = 0; k < ALBN; ++k) {
+                    const int idx = c + k * NFUSE * 32;
+                    if (idx < ALBQ) {
+                        const int ch = idx / (TH * (TW / 4)), rem = idx - ch * (TH * (TW / 4));
+                        const int r = rem / (TW / 4), q = rem - r * (TW / 4);
+                        float4* sp = reinterpret_cast<float4*>(&sm.stage[ch][r][4 * q]);
+                        const float4 v = *sp, a = albv[k];
+                        *sp = make_float4(v.x * a.x, v.y * a.y, v.z * a.z, v.w * a.w);
                     }
                 }
             }
