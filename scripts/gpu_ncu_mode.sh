@@ -3,7 +3,7 @@
 MODE=$1; TAG=$2
 cd $GRAFT_REPO_ROOT
 case $MODE in
-  bwd) K='regex:fused_tma|bwd_'; N=3 ;;
+  bwd) K='regex:lse_kernel|fused_tma|bwd_'; N=4 ;;
   mr) K='regex:down4|fused_tma|combine'; N=6 ;;
   temporal) K='regex:temporal'; N=1 ;;
 esac
