@@ -130,3 +130,9 @@ def test_binding_bf16_dtype_checks(kmdmod):
     x = torch.zeros(1, 3, 8, 8)
     with pytest.raises(ValueError, match="CUDA"):
         kmdmod.decode_filter_fuse(x, torch.zeros(1, 1, 8, 8, dtype=torch.bfloat16), None, [3])
+
+
+def test_backward_workspace_formula(kmdmod):
+    # kmd.h: 8 M + 4 bytes per pixel (the (s_i, d_i) pairs and the log-sum-exp plane)
+    for N, H, W, sizes in [(1, 1080, 1920, [3, 5, 7, 9, 11, 13]), (2, 64, 96, [3, 5]), (1, 8, 8, [3])]:
+        assert kmdmod.backward_workspace_bytes(N, H, W, sizes) == N * H * W * (8 * len(sizes) + 4)
