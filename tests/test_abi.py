@@ -136,3 +136,18 @@ def test_backward_workspace_formula(kmdmod):
     # kmd.h: 8 M + 4 bytes per pixel (the (s_i, d_i) pairs and the log-sum-exp plane)
     for N, H, W, sizes in [(1, 1080, 1920, [3, 5, 7, 9, 11, 13]), (2, 64, 96, [3, 5]), (1, 8, 8, [3])]:
         assert kmdmod.backward_workspace_bytes(N, H, W, sizes) == N * H * W * (8 * len(sizes) + 4)
+
+
+def test_header_is_plain_c99(tmp_path):
+    # the boundary is a C ABI: include/kmd.h compiles as strict C99 (no C++ or torch types)
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not found")
+    src = tmp_path / "h.c"
+    src.write_text('#include "kmd.h"\nint main(void) { kmd_config c; (void)c; return 0; }\n')
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic",
+                        "-I", os.path.join(ROOT, "include"), "-c", str(src), "-o", str(tmp_path / "h.o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
