@@ -390,6 +390,63 @@ def test_mr_single_level_is_plain_decoder(oracle_mod):
     assert np.array_equal(a, b)
 
 
+def _mr_level_inputs(H, W, sizes, rng):
+    imps, blends = [], []
+    for l, s in enumerate(sizes):
+        _, i, b = _rand_inputs(H >> l, W >> l, len(s), rng)
+        imps.append(i)
+        blends.append(b)
+    return imps, blends
+
+
+def test_mr_three_levels_alpha_zero_is_level0_decoder(oracle_mod):
+    # Eq. 7 with alpha = 0 everywhere: o = f at every level, so the output is
+    # level 0's plain decoder (reading R18)
+    H, W, sizes = 24, 32, [[3, 5], [3, 5], [3, 5]]
+    rad, _, _ = _rand_inputs(H, W, 1, RNG)
+    imps, blends = _mr_level_inputs(H, W, sizes, RNG)
+    alphas = [np.zeros((1, 1, H >> l, W >> l), np.float32) for l in range(2)]
+    a = oracle_mod.mr_decode_filter_fuse(rad, imps, blends, alphas, sizes)
+    b = oracle_mod.decode_filter_fuse(rad, imps[0], blends[0], sizes[0])
+    assert np.array_equal(a, b)
+
+
+def test_mr_three_levels_constant_radiance_exact(oracle_mod):
+    # every level reproduces a constant (to fp64 rounding, exactly after fp32
+    # rounding) and D, U keep it, so f + alpha (U c - U D f) = K for any alpha
+    H, W, sizes = 24, 32, [[3, 5], [3, 7], [5, 3]]
+    rad = np.full((1, 3, H, W), 0.375, np.float32)
+    imps, blends = _mr_level_inputs(H, W, sizes, RNG)
+    alphas = [RNG.uniform(0, 1, (1, 1, H >> l, W >> l)).astype(np.float32) for l in range(2)]
+    out = oracle_mod.mr_decode_filter_fuse(rad, imps, blends, alphas, sizes)
+    np.testing.assert_allclose(out, 0.375, rtol=1e-14, atol=0)
+    assert np.all(out.astype(np.float32) == np.float32(0.375))
+
+
+def test_mr_two_levels_uniform_importance_is_scipy_pyramid(oracle_mod):
+    # Uniform importance turns every level into a clamp-to-edge box mean
+    # (pinned above), so a two-level M = 1 "Ours MR" is, written with scipy and
+    # numpy only: f = box_3(r), c = box_5(fp32(D r)) (R19), o = f + a (U c - U D f)
+    H, W = 12, 20
+    rad = RNG.exponential(1.0, (1, 3, H, W)).astype(np.float32)
+    imps = [np.zeros((1, 1, H, W), np.float32), np.zeros((1, 1, H // 2, W // 2), np.float32)]
+    alpha = RNG.uniform(0, 1, (1, 1, H, W)).astype(np.float32)
+    out = oracle_mod.mr_decode_filter_fuse(rad, imps, None, [alpha], [[3], [5]])
+
+    def D(x):
+        return x.reshape(x.shape[0], x.shape[1], x.shape[2] // 2, 2, x.shape[3] // 2, 2).mean(axis=(3, 5))
+
+    def U(x):
+        return np.repeat(np.repeat(x, 2, axis=2), 2, axis=3)
+
+    r64 = rad.astype(np.float64)
+    f = np.stack([_box(r64[0, c], 3) for c in range(3)])[None]
+    dr = D(r64).astype(np.float32).astype(np.float64)
+    cc = np.stack([_box(dr[0, c], 5) for c in range(3)])[None]
+    ref = f + alpha.astype(np.float64) * (U(cc) - U(D(f)))
+    np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
 # ------------------------------------------------------ backward (NEXT row 3)
 def _torch_forward_fp64(rad, imp, blend, sizes, logits=True):
     """Eq. 3-5 written with torch library steps (replicate pad + F.unfold,
