@@ -74,15 +74,27 @@ constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to f
 // alternative: the network's low-precision output) -- IN16 below.  A bf16 row
 // of the importance box is 72 elements (144 bytes: TMA rows are multiples of
 // 16 bytes); the logit box stays 56 wide (112 bytes).
+// Fusion thread -> (row, segment) map (KMD_ROWMAP, 27-row tiles): a warp's
+// 4 row groups are rows of one parity, 2 apart (warps 2m, 2m+1 cover rows
+// 8m .. 8m+7; the last warp rows 24-26).  Row offsets of the staged tile are
+// then 0, 8, 16, 24 banks (52-float rows), so with the segment starts below
+// the epilogue's stage stores are conflict-free (consecutive rows: 2-way);
+// the fp32 blend box is 60 wide so its rows stay 8 banks apart as well.
+#ifndef KMD_ROWMAP
+#define KMD_ROWMAP 1
+#endif
+constexpr bool ROWMAP = KMD_ROWMAP && TH == 27;
 template <bool IN16>
 struct InElem {
     using T = float;
     static constexpr int IW = BW;
+    static constexpr int BBW = ROWMAP ? 60 : 56;  // blend box width (multiple of 4: 16-byte TMA rows)
 };
 template <>
 struct InElem<true> {
     using T = unsigned short;  // bf16 bits
     static constexpr int IW = 72;
+    static constexpr int BBW = 56;                // 112-byte rows
 };
 __device__ __forceinline__ float ld_in(const float* q) { return *q; }
 __device__ __forceinline__ float ld_in(const unsigned short* q) { return __uint_as_float((unsigned)*q << 16); }
@@ -101,13 +113,13 @@ struct InSlotT {
 struct alignas(128) Slot {
     float4 V[TH][VS];                  // vertical box sums of (e, e r, e g, e b), by field column
 };
-// blend box: the 52 output columns plus 4 of padding, starting at x0 (no
-// halo); the 56-element row stride puts the 4 rows x 8 segment starts a fusion
-// warp reads at 32 distinct banks (fp32)
-constexpr int BBW = 56;
+// blend box: the 52 output columns plus padding, starting at x0 (no halo);
+// the row stride (fp32: 60 with ROWMAP's rows 2 apart, 56 with consecutive
+// rows) puts the 4 rows x 8 segment starts a fusion warp reads at 32 distinct
+// banks
 template <bool IN16>
 struct BSlotT {
-    alignas(128) typename InElem<IN16>::T B[TH][BBW];  // blend logits of map i, rows y0 .. y0+26, cols x0 .. x0+55
+    alignas(128) typename InElem<IN16>::T B[TH][InElem<IN16>::BBW];  // blend logits of map i, rows y0 .. y0+26, cols x0 .. x0+55
 };
 struct RadBuf {
     alignas(128) float v[3][FH][BW];   // radiance r, g, b; same box as I
@@ -123,6 +135,7 @@ struct SmemT {
         b_empty[NB];
 };
 using Smem = SmemT<false>;
+static_assert(sizeof(SmemT<false>) <= 232448 && sizeof(SmemT<true>) <= 232448, "227 KB of shared memory per CTA");
 static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlotT<false>) % 128 == 0 &&
                   sizeof(BSlotT<false>) % 128 == 0 && sizeof(InSlotT<true>) % 128 == 0 &&
                   sizeof(BSlotT<true>) % 128 == 0,
@@ -446,7 +459,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             constexpr unsigned ESZ = SP::IN16 ? 2 : 4;
             constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * InElem<SP::IN16>::IW * ESZ,
-                               B_BYTES = TH * BBW * ESZ;
+                               B_BYTES = TH * InElem<SP::IN16>::BBW * ESZ;
             // In-order, blocking issue of every (tile, size) step: radiance
             // (per tile), importance and blend logits.  Deadlock-free: each wait
             // is on a slot released by a step whose inputs were issued earlier
@@ -547,7 +560,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // lanes of a row hit 8 different 16-byte bank groups with every
         // LDS.128 of V.  Every thread computes 7 pixels (the 7th of a 6-pixel
         // segment is recomputed by its neighbour and not stored).
-        const int ty = c / NSEG, sub = c % NSEG;
+        const int sub = c % NSEG;
+        const int ty = ROWMAP ? ((c >> 5) < 6 ? 8 * (c >> 6) + ((c >> 5) & 1) + 2 * ((c >> 3) & 3) : 24 + ((c >> 3) & 3))
+                              : c / NSEG;
         const bool active = ty < TH;  // the last fusion warp may have spare lanes
         const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
         const int len = (0x76677766u >> (4 * sub)) & 0xf;
@@ -828,7 +843,8 @@ cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream) {
         !make_map(&m_out, ws, p.W, p.H, 2LL * p.M * p.N, TW, TH, 2))
         return cudaErrorInvalidValue;
     if (p.blend) {
-        if (!make_map(&m_blend, p.blend, p.W, p.H, (long long)p.M * p.N, BBW, TH, 1)) return cudaErrorInvalidValue;
+        if (!make_map(&m_blend, p.blend, p.W, p.H, (long long)p.M * p.N, InElem<false>::BBW, TH, 1))
+            return cudaErrorInvalidValue;
     } else {
         m_blend = m_imp;
     }
@@ -868,7 +884,8 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
         !make_map(&m_out, p.out, p.W, p.out_rows, 3LL * p.N, TW, TH, 3))
         return cudaErrorInvalidValue;
     if (p.blend) {
-        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N, BBW, TH, 1, b16))
+        if (!make_map(&m_blend, p.blend, p.W, p.out_rows, (long long)p.M * p.N,
+                      b16 ? InElem<true>::BBW : InElem<false>::BBW, TH, 1, b16))
             return cudaErrorInvalidValue;
     } else {
         m_blend = m_imp;  // never used
