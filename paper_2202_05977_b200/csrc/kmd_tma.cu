@@ -84,6 +84,26 @@ constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to f
 #define KMD_ROWMAP 1
 #endif
 constexpr bool ROWMAP = KMD_ROWMAP && TH == 27;
+// output row of fusion thread c (0 .. 32 NFUSE - 1; its segment is c % NSEG);
+// rows >= TH are idle lanes
+__host__ __device__ constexpr int fuse_row(int c) {
+    return ROWMAP ? ((c >> 5) < 6 ? 8 * (c >> 6) + ((c >> 5) & 1) + 2 * ((c >> 3) & 3) : 24 + ((c >> 3) & 3))
+                  : c / NSEG;
+}
+// every (row, segment) of the tile has exactly one fusion thread
+constexpr bool fuse_map_is_bijective() {
+    unsigned segs[32] = {};
+    for (int c = 0; c < 32 * ((TH * NSEG + 31) / 32); ++c) {
+        const int r = fuse_row(c);
+        if (r >= TH) continue;
+        if (segs[r] & (1u << (c % NSEG))) return false;
+        segs[r] |= 1u << (c % NSEG);
+    }
+    for (int r = 0; r < TH; ++r)
+        if (segs[r] != (1u << NSEG) - 1) return false;
+    return true;
+}
+static_assert(TH <= 32 && fuse_map_is_bijective(), "fusion thread map covers each tile row with 8 segments");
 template <bool IN16>
 struct InElem {
     using T = float;
@@ -561,8 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // LDS.128 of V.  Every thread computes 7 pixels (the 7th of a 6-pixel
         // segment is recomputed by its neighbour and not stored).
         const int sub = c % NSEG;
-        const int ty = ROWMAP ? ((c >> 5) < 6 ? 8 * (c >> 6) + ((c >> 5) & 1) + 2 * ((c >> 3) & 3) : 24 + ((c >> 3) & 3))
-                              : c / NSEG;
+        const int ty = fuse_row(c);
         const bool active = ty < TH;  // the last fusion warp may have spare lanes
         const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
         const int len = (0x76677766u >> (4 * sub)) & 0xf;
