@@ -33,10 +33,20 @@
  *  - Aliasing: `out` must not overlap any input (the stencil reads
  *    neighbours) -> KMD_ERR_ALIAS.
  *  - Numerics: max relative error <= 1e-5 against the fp64 oracle for finite
- *    inputs with radiance >= 0.  Importance values are used
- *    unshifted (exp(I)) while a tile's values lie in [KMD_EXP_SAFE_LO,
- *    KMD_EXP_SAFE_HI] and |radiance| <= KMD_RADIANCE_SAFE; otherwise that tile
- *    takes a per-window max-shifted path (same result, slower).
+ *    inputs with radiance >= 0.  Every kernel evaluates Eq. 3
+ *    with unshifted exp(I) (any shift cancels, reading R2) and guards the
+ *    range as follows (reading R13):
+ *      TMA kernel (W % 4 == 0, 16-B aligned, k <= 13; kmd_last_kernel() 3,
+ *      100+M, 150+M, 200+M): per output PIXEL.  A pixel is recomputed by a
+ *      per-window max-shifted evaluation (IEEE expf and division) when, for
+ *      any size, its box denominator sum_q exp(I(q)) lies outside
+ *      [1e-30, 1e36] (this includes overflow to +inf), when the sum of its
+ *      fusion weights exp(B_i) lies outside [1e-30, 1e30], or when its result
+ *      is not finite.
+ *      Other kernels (kmd_last_kernel() 1, 2): per (tile, size).  A tile whose
+ *      importance values leave [KMD_EXP_SAFE_LO, KMD_EXP_SAFE_HI] or whose
+ *      |radiance| exceeds KMD_RADIANCE_SAFE takes the max-shifted path.
+ *    Either way the result is the same operation; only the speed differs.
  */
 #ifndef KMD_H
 #define KMD_H

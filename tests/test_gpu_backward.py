@@ -7,8 +7,8 @@ test_oracle_pins.py).
 Tolerance (backward): dL/dI_i(q) = e(q)[sum_c r_c T_c - T_R]
 is a difference of two fp32 box-transposed sums of similar size, so its
 error is relative to the map's scale, not to each element: we require
-|gpu - ref| <= BWD_TOL * max|ref| over each (frame, size) map, BWD_TOL = 1e-4
-(~1000 ulp: two k-tap fp32 sums per axis, a division and the cancellation).
+|gpu - ref| <= BWD_TOL * max|ref| over each (frame, size) map, BWD_TOL = 1e-5,
+north_star's bar applied normwise (measured 1e-7 .. 1.3e-6 in round 1).
 """
 import numpy as np
 import pytest
@@ -19,7 +19,7 @@ from paper_2202_05977_b200 import kmd
 
 pytestmark = pytest.mark.gpu
 PAPER = list(gen.PAPER_SIZES)
-BWD_TOL = 1e-4
+BWD_TOL = 1e-5
 
 
 def _normwise(gpu, ref, what):
