@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--rotate", type=int, default=4, help="distinct resident frames per rank")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--batch", type=int, default=256,
-                    help="--mode batch: frames per rank in one launch (BASELINE.json configs[4])")
+                    help="--mode batch: frames in the whole batch, sharded over the ranks (BASELINE.json configs[4])")
     ap.add_argument("--albedo", action="store_true",
                     help="NEXT row 1: fuse the albedo remodulation epilogue (out = Rhat * albedo)")
     ap.add_argument("--bf16", action="store_true",
@@ -180,6 +180,18 @@ def recorded_traffic(workload: str):
 
 
 # ----------------------------------------------------------------- oracle legs
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu / /proc/cpuinfo), for cpu_baseline."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_rows_time(inp_cpu, sizes, rows, threads=0):
     import oracle
     t0 = time.perf_counter()
@@ -229,7 +241,7 @@ def run_reference(args, rank, world):
         "config": {"workload": f"{W}x{H} frame, sizes {sizes}, fusion (configs[2])",
                    "global_batch": 1, "parallelism": "host OpenMP"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -369,7 +381,7 @@ def run_kmd(args, rank, world, local):
         r1 = max(1, min(8, rows))
         dt1, _ = oracle_rows_time(inp_cpu, sizes, (y0, y0 + r1), threads=1)
         cpu = {"value": rows * W / dt / 1e6, "unit": UNIT, "cores": oracle.max_threads(),
-               "kind": "oracle",
+               "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"rows {y0}..{y0 + rows} ({rows * W} px) of frame 0 of the {W}x{H} "
                          f"M={M} workload, fp64 oracle, {dt:.1f} s",
                "value_1thread": r1 * W / dt1 / 1e6,
@@ -417,10 +429,13 @@ def run_kmd(args, rank, world, local):
 
 
 def run_band(args, rank, world, local):
-    """configs[3]: one 3840x2160 frame per step, split into `world` row bands.
-    Each step exchanges the r_max halo rows of the radiance and importance
-    planes with the neighbouring ranks (torch.distributed P2P = NCCL over
-    NVLink) and runs kmd_decode_filter_fuse_band on the rank's band."""
+    """configs[3]: one 3840x2160 frame per step, split into `world` row bands
+    (strong scaling).  Each step is libkmd's kmd_band_step: the r_max halo rows
+    of the 3 radiance and M importance planes go to / come from the
+    neighbouring ranks in ONE grouped NCCL call on a side stream (libkmd's own
+    communicator, its unique id broadcast over torch.distributed), while the
+    band's interior tile rows run on the compute stream; the seam tile rows
+    follow the exchange.  At N = 1 it is the whole 4K frame on one GPU."""
     from paper_2202_05977_b200 import bands as B
     from paper_2202_05977_b200 import inputs as gen
     from paper_2202_05977_b200 import kmd
@@ -431,24 +446,33 @@ def run_band(args, rank, world, local):
     M = len(sizes)
     F = 2
     K, Wm = args.steps, args.warmup
+    assert Wm >= 3, "timing rules: at least 3 warm-up steps"
     kmd.lib()
     band = B.split_rows(H, world, sizes)[rank]
+    r = B.rmax_of(sizes)
+    up = rank - 1 if band.halo_top > 0 else -1
+    down = rank + 1 if band.halo_bot > 0 else -1
     full = gen.make_inputs(F, H, W, M, device=dev)      # identical on every rank (same seeds)
     rad = [B.slice_band(full.radiance[f:f + 1], band) for f in range(F)]
     imp = [B.slice_band(full.importance[f:f + 1], band) for f in range(F)]
     bl = [full.blend[f:f + 1, :, band.y0:band.y0 + band.rows].contiguous() for f in range(F)]
     out = torch.empty((1, 3, band.rows, W), device=dev)
     del full
+    comm = B.make_comm() if world > 1 else None
+    side = torch.cuda.Stream(dev)
+    stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize(dev)
 
     def step(s):
         f = s % F
-        if world > 1:
-            B.exchange_halos(rad[f], band, world)
-            B.exchange_halos(imp[f], band, world)
-        kmd.decode_filter_fuse_band(rad[f], imp[f], bl[f], sizes, y0=band.y0, band_rows=band.rows,
-                                    halo_top=band.halo_top, halo_bot=band.halo_bot, H_global=H,
-                                    out=out)
+        kmd.band_step(comm, rad[f], imp[f], bl[f], sizes, out, y0=band.y0, band_rows=band.rows, halo=r,
+                      peer_up=up, peer_down=down, H_global=H, stream=stream, comm_stream=side)
+
+    def kernel_only(s):
+        f = s % F
+        kmd.decode_filter_fuse_band_part(rad[f], imp[f], bl[f], sizes, kmd.BAND_ALL, y0=band.y0,
+                                         band_rows=band.rows, halo_top=band.halo_top,
+                                         halo_bot=band.halo_bot, H_global=H, out=out, stream=stream)
 
     for s in range(Wm):
         step(s)
@@ -456,27 +480,51 @@ def run_band(args, rank, world, local):
     barrier(world)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        a.record()
+        a.record(stream)
         for s in range(K):
             step(s)
-        b.record()
+        b.record(stream)
         torch.cuda.synchronize(dev)
     barrier(world)
     el = max_over_ranks(a.elapsed_time(b), world)
+    # the band kernel alone (no exchange), for the roofline: same buffers
+    Kk = min(K, 200)
+    for s in range(3):
+        kernel_only(s)
+    torch.cuda.synchronize(dev)
+    a.record(stream)
+    for s in range(Kk):
+        kernel_only(s)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    kern_ms = a.elapsed_time(b) / Kk
+    kind = kmd.last_kernel()
+    if comm is not None:
+        comm.destroy()
     if rank != 0:
         return
     value = H * W * K / (el / 1e3) / 1e6
-    halo_bytes = 2 * 6 * W * (3 + M) * 4 if world > 1 else 0
+    halo_bytes = r * W * (3 + M) * 4 if world > 1 else 0
+    algo = kmd.algorithmic_bytes(1, band.rows, W, sizes, True)
+    peak, peak_src = measured_peak_hbm()
+    achieved = algo / (kern_ms / 1e3) / 1e9
     print(json.dumps({
         "metric": f"{W}x{H} Mpix/s (decode+filter+fusion, row bands)", "value": value, "unit": UNIT,
         "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": el / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{W}x{H} frame split into {world} row bands + NCCL halo exchange "
                                f"(BASELINE.json configs[3])", "sizes": sizes,
-                   "band_rows": band.rows, "halo_bytes_per_seam": halo_bytes,
-                   "parallelism": f"row bands x{world}"},
-        "clocks": clk.summary(), "gpu_launches": K * kmd.launches_per_call(),
-        "timing": "CUDA events around K eager steps (exchange + band kernel), max over ranks"}),
+                   "band_rows": band.rows, "halo_bytes_per_seam_per_direction": halo_bytes,
+                   "parallelism": f"row bands x{world}",
+                   "l2": f"inputs rotate over {F} frames ({F * algo * world / 1e6:.0f} MB > 126 MB L2)"},
+        "kernel_ms": {"avg": kern_ms, "how": f"CUDA events around {Kk} band launches without the exchange "
+                                             f"(rank 0's band, {band.rows} rows)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "algorithmic_bytes_per_launch": algo,
+                     "peak_source": peak_src, "kernel": f"band kernel (libkmd, {kind})"},
+        "clocks": clk.summary(), "gpu_launches": K * (1 if world == 1 else 2),
+        "timing": "CUDA events around K steps (kmd_band_step: NCCL exchange on a side stream overlapped "
+                  "with the interior, then the seams), max over ranks"}),
         flush=True)
 
 
@@ -734,21 +782,25 @@ def run_sweep(args, rank, world, local):
 
 
 def run_batch(args, rank, world, local):
-    """BASELINE.json configs[4]: a batch of B 1080p frames per rank in ONE launch
-    (frame-parallel, no data-path collective; weak scaling over ranks)."""
+    """BASELINE.json configs[4]: a batch of --batch (256) 1080p frames sharded
+    across the ranks (rank g takes frames [g B / N, (g+1) B / N), one launch per
+    rank per step; no data-path collective).  The total batch is fixed as N
+    grows: strong scaling of the batch."""
     from paper_2202_05977_b200 import inputs as gen
     from paper_2202_05977_b200 import kmd
     dev = torch.device("cuda", local)
-    H, W, B = args.height, args.width, args.batch
+    H, W, Bg = args.height, args.width, args.batch
+    f0, f1 = rank * Bg // world, (rank + 1) * Bg // world
+    B = f1 - f0
     sizes = [int(x) for x in args.sizes.split(",")]
     M = len(sizes)
-    # B distinct frames resident (frame ids rank*B ..): generated in chunks
+    # this rank's shard of the batch resident (global frame ids f0 .. f1-1): generated in chunks
     rad = torch.empty((B, 3, H, W), device=dev)
     imp = torch.empty((B, M, H, W), device=dev)
     bl = torch.empty((B, M, H, W), device=dev) if M > 1 else None
     for c0 in range(0, B, 16):
         n = min(16, B - c0)
-        x = gen.make_inputs(n, H, W, M, frame_offset=rank * B + c0, device=dev)
+        x = gen.make_inputs(n, H, W, M, frame_offset=f0 + c0, device=dev)
         rad[c0:c0 + n], imp[c0:c0 + n] = x.radiance, x.importance
         if bl is not None:
             bl[c0:c0 + n] = x.blend
@@ -771,23 +823,26 @@ def run_batch(args, rank, world, local):
         b.record()
         torch.cuda.synchronize(dev)
     barrier(world)
-    el = max_over_ranks(a.elapsed_time(b), world)
+    el_local = a.elapsed_time(b)
+    el = max_over_ranks(el_local, world)
     if rank != 0:
         return
     ms = el / K
     algo = kmd.algorithmic_bytes(B, H, W, sizes, bl is not None)
     peak = measured_peak_hbm()[0]
     print(json.dumps({
-        "metric": f"{W}x{H} Mpix/s, batch of {B} frames per GPU in one launch", "value": B * H * W * world * K / (el / 1e3) / 1e6,
+        "metric": f"{W}x{H} Mpix/s, batch of {Bg} frames sharded over the GPUs", "value": Bg * H * W * K / (el / 1e3) / 1e6,
         "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"batch {B} x {W}x{H}, sizes {sizes} (BASELINE.json configs[4])",
-                   "global_batch": B * world, "resident_gb": round((rad.numel() + imp.numel() + out.numel() + (bl.numel() if bl is not None else 0)) * 4 / 1e9, 1),
-                   "parallelism": f"frame-parallel x{world} (no data-path collective)"},
-        "ms_per_frame": ms / B,
-        "roofline": {"bound": "hbm", "achieved": algo / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": algo / (ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo,
-                     "kernel": kmd.last_kernel()},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"batch {Bg} x {W}x{H}, sizes {sizes} (BASELINE.json configs[4])",
+                   "global_batch": Bg, "frames_per_rank": B,
+                   "resident_gb_per_rank": round((rad.numel() + imp.numel() + out.numel() + (bl.numel() if bl is not None else 0)) * 4 / 1e9, 1),
+                   "parallelism": f"frame-parallel x{world} (no data-path collective)",
+                   "l2": "inputs of one step >> 126 MB L2"},
+        "ms_per_frame": ms / Bg,
+        "roofline": {"bound": "hbm", "achieved": algo / (el_local / K / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": algo / (el_local / K / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo,
+                     "traffic": None, "kernel": f"{kmd.last_kernel()} on rank 0's {B} frames"},
         "clocks": clk.summary(), "gpu_launches": K}), flush=True)
 
 

@@ -78,7 +78,7 @@ typedef enum {
                            16-byte aligned (the fp32 entry points accept any 4-byte pointer)  */
     KMD_ERR_ALIAS = 5,  /* out overlaps an input                                              */
     KMD_ERR_CUDA = 6,   /* a CUDA runtime call or launch failed (see kmd_last_error)          */
-    KMD_ERR_NCCL = 7    /* reserved for collective helpers                                    */
+    KMD_ERR_NCCL = 7    /* NCCL unavailable or an NCCL call failed (kmd_halo_exchange etc.) */
 } kmd_status;
 
 typedef enum { KMD_BORDER_CLAMP = 0 } kmd_border;
@@ -171,6 +171,80 @@ kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* impor
                                        int32_t band_rows, int32_t W, int32_t halo_top,
                                        int32_t halo_bot, int32_t y0, int32_t H_global,
                                        const kmd_config* cfg, kmd_stream_t stream);
+
+/* The band call in two parts, so the halo exchange can overlap the work that
+ * does not need it.  part = KMD_BAND_ALL: the whole band
+ * (== kmd_decode_filter_fuse_band).  KMD_BAND_INTERIOR: only the output rows
+ * whose windows read owned rows alone (rows [y0, y0 + band_rows), plus frame
+ * edges clamped where halo_top / halo_bot is 0); the halo rows of radiance and
+ * importance are not read and may be in flight.  KMD_BAND_SEAMS: every other
+ * output row of the band (the rows next to a non-empty halo).  INTERIOR then
+ * SEAMS write every output row exactly once, bitwise equal to KMD_BAND_ALL.
+ * The split follows the TMA kernel's global tile grid; when
+ * another kernel serves the band (W % 4 != 0, unaligned, k > 13), INTERIOR
+ * does nothing and SEAMS does the whole band.  Arguments and errors as
+ * kmd_decode_filter_fuse_band; part outside these values -> KMD_ERR_CONFIG. */
+#define KMD_BAND_ALL 0
+#define KMD_BAND_INTERIOR 1
+#define KMD_BAND_SEAMS 2
+kmd_status kmd_decode_filter_fuse_band_part(const float* radiance, const float* importance,
+                                            const float* blend, float* out, int32_t N,
+                                            int32_t band_rows, int32_t W, int32_t halo_top,
+                                            int32_t halo_bot, int32_t y0, int32_t H_global,
+                                            const kmd_config* cfg, int32_t part, kmd_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU row bands over NCCL (configs[3]): one process per
+ * GPU, one communicator over the ranks that share a frame.  libkmd loads NCCL
+ * at run time (dlopen "libnccl.so.2"; in a process that imported torch this is
+ * torch's NCCL); without it these calls return KMD_ERR_NCCL and nothing else
+ * in the library is affected.
+ *
+ * kmd_nccl_unique_id: rank 0 creates the 128-byte id (NCCL_UNIQUE_ID_BYTES),
+ *   which the caller broadcasts to every rank (e.g. torch.distributed).
+ * kmd_comm_init: collective over nranks processes (blocking); *comm receives an
+ *   opaque handle (an ncclComm_t) owned by the caller until kmd_comm_destroy.  */
+#define KMD_NCCL_ID_BYTES 128
+kmd_status kmd_nccl_unique_id(uint8_t id[KMD_NCCL_ID_BYTES]);
+kmd_status kmd_comm_init(void** comm, const uint8_t id[KMD_NCCL_ID_BYTES], int32_t nranks, int32_t rank);
+kmd_status kmd_comm_destroy(void* comm);
+
+/* Halo exchange of one row band: ONE grouped NCCL step (ncclGroupStart /
+ * ncclGroupEnd) over every plane, posted directly on the halo and edge rows
+ * (each a contiguous [rows][W] block of its plane; no staging copies).
+ *   planes[p]   host array of n_planes device pointers; plane p is fp32
+ *               [halo_top + band_rows + halo_bot][W], owned rows filled
+ *   halo        rows exchanged with each neighbour (r_max of the band call)
+ *   peer_up     rank owning the rows above (its last rows are our top halo), or -1
+ *   peer_down   rank owning the rows below, or -1
+ *   halo_top = peer_up >= 0 ? halo : 0, halo_bot = peer_down >= 0 ? halo : 0.
+ * Per plane, in this order: recv rows [0, halo_top) from peer_up; recv rows
+ * [halo_top + band_rows, + halo_bot) from peer_down; send rows
+ * [halo_top, halo_top + halo) to peer_up; send rows
+ * [halo_top + band_rows - halo, halo_top + band_rows) to peer_down.  NCCL
+ * matches the messages of one pair of ranks in posting order, so a rank that
+ * is its own neighbour (peer == its rank) receives its first owned rows into
+ * its top halo and its last owned rows into its bottom halo.
+ * Enqueued on stream; band_rows >= halo >= 0 (else KMD_ERR_DIM); NCCL failures
+ * -> KMD_ERR_NCCL.                                                            */
+kmd_status kmd_halo_exchange(void* comm, float* const* planes, int32_t n_planes, int32_t band_rows,
+                             int32_t W, int32_t halo, int32_t peer_up, int32_t peer_down,
+                             kmd_stream_t stream);
+
+/* One band step with the exchange overlapped: the exchange
+ * of the 3 radiance and M importance planes of every frame runs on
+ * comm_stream while the band interior (KMD_BAND_INTERIOR) runs on stream; the
+ * seams (KMD_BAND_SEAMS) follow once the exchange is complete.  Buffers as
+ * kmd_decode_filter_fuse_band with halo_top / halo_bot derived from halo and
+ * the peers as in kmd_halo_exchange (radiance and importance are written:
+ * their halo rows).  comm_stream == stream (or NULL) serialises the exchange
+ * before the interior.  comm may be NULL when both peers are -1.  All work is
+ * ordered after what was queued on stream and before what is queued on it
+ * afterwards.                                                                */
+kmd_status kmd_band_step(void* comm, float* radiance, float* importance, const float* blend, float* out,
+                         int32_t N, int32_t band_rows, int32_t W, int32_t halo, int32_t peer_up,
+                         int32_t peer_down, int32_t y0, int32_t H_global, const kmd_config* cfg,
+                         kmd_stream_t stream, kmd_stream_t comm_stream);
 
 /* End-to-end from HOST memory: copies the inputs host->device, runs the fused
  * kernel and copies the result device->host, all on `stream` (pinned host

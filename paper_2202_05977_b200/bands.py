@@ -61,33 +61,47 @@ def slice_band(full: torch.Tensor, band: Band) -> torch.Tensor:
 
 def exchange_halos(buf: torch.Tensor, band: Band, world: int, group=None) -> None:
     """Fill the halo rows of ``buf`` ([N,C,buf_rows,W], owned rows already set)
-    from the neighbouring ranks.  One grouped send/recv step (batch_isend_irecv):
-    my first rows go to rank-1 (its bottom halo), my last rows to rank+1 (its
-    top halo); neighbours' rows land in my halos."""
+    from the neighbouring ranks in one grouped send/recv step
+    (batch_isend_irecv), posted directly on each plane's halo / edge rows (a
+    contiguous [rows, W] block of the plane; no staging copies).  Same order
+    and meaning as libkmd's kmd_halo_exchange (include/kmd.h), which does this
+    over NCCL on GPUs: my first rows go to rank-1 (its bottom halo), my last
+    rows to rank+1 (its top halo); neighbours' rows land in my halos."""
     import torch.distributed as dist
 
+    assert buf.is_contiguous()
     r = band.rank
-    ops, recvs = [], []
     own0, own1 = band.halo_top, band.halo_top + band.rows
-    if r > 0 and band.halo_top > 0:
-        n_up = _peer_halo_bot(band)
-        send_up = buf[:, :, own0:own0 + n_up].contiguous()
-        recv_top = torch.empty_like(buf[:, :, 0:band.halo_top])
-        ops.append(dist.P2POp(dist.isend, send_up, r - 1, group))
-        ops.append(dist.P2POp(dist.irecv, recv_top, r - 1, group))
-        recvs.append((recv_top, 0))
-    if r < world - 1 and band.halo_bot > 0:
-        n_down = _peer_halo_top(band)
-        send_down = buf[:, :, own1 - n_down:own1].contiguous()
-        recv_bot = torch.empty_like(buf[:, :, own1:own1 + band.halo_bot])
-        ops.append(dist.P2POp(dist.isend, send_down, r + 1, group))
-        ops.append(dist.P2POp(dist.irecv, recv_bot, r + 1, group))
-        recvs.append((recv_bot, own1))
+    up = r > 0 and band.halo_top > 0
+    down = r < world - 1 and band.halo_bot > 0
+    ops = []
+    N, C = buf.shape[0], buf.shape[1]
+    for n in range(N):
+        for c in range(C):
+            pl = buf[n, c]
+            if up:
+                ops.append(dist.P2POp(dist.irecv, pl[0:band.halo_top], r - 1, group))
+            if down:
+                ops.append(dist.P2POp(dist.irecv, pl[own1:own1 + band.halo_bot], r + 1, group))
+            if up:
+                ops.append(dist.P2POp(dist.isend, pl[own0:own0 + _peer_halo_bot(band)], r - 1, group))
+            if down:
+                ops.append(dist.P2POp(dist.isend, pl[own1 - _peer_halo_top(band):own1], r + 1, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    for t, row in recvs:
-        buf[:, :, row:row + t.shape[2]].copy_(t)
+
+
+def make_comm(group=None):
+    """libkmd NCCL communicator over the ranks of ``group`` (torch.distributed
+    initialised): rank 0's kmd_nccl_unique_id is broadcast to every rank."""
+    import torch.distributed as dist
+
+    from . import kmd
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = [kmd.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    return kmd.Comm(uid[0], world, rank)
 
 
 def _peer_halo_bot(band: Band) -> int:

@@ -28,6 +28,22 @@ kmd_status fail(kmd_status s, const char* fmt, ...) {
     return s;
 }
 
+}  // namespace
+
+namespace kmd {
+// the error detail of the other translation units (kmd_band.cu)
+kmd_status api_fail(kmd_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+void api_clear_error() { g_err[0] = 0; }
+}  // namespace kmd
+
+namespace {
+
 kmd_status cuda_fail(cudaError_t e, const char* what) {
     return fail(KMD_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
@@ -238,12 +254,16 @@ kmd_status kmd_fuse(const float* filtered, const float* blend, float* out, int32
     return KMD_OK;
 }
 
-kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* importance,
-                                       const float* blend, float* out, int32_t N,
-                                       int32_t band_rows, int32_t W, int32_t halo_top,
-                                       int32_t halo_bot, int32_t y0, int32_t H_global,
-                                       const kmd_config* cfg, kmd_stream_t stream) {
-    g_err[0] = 0;
+}  // extern "C"
+
+namespace {
+
+// Validates a row band and fills its launch parameters (the checks of
+// kmd_decode_filter_fuse_band).  Returns KMD_OK with *skip = true when N == 0.
+kmd_status band_params(const float* radiance, const float* importance, const float* blend, float* out, int32_t N,
+                       int32_t band_rows, int32_t W, int32_t halo_top, int32_t halo_bot, int32_t y0,
+                       int32_t H_global, const kmd_config* cfg, kmd::FusedParams* p, bool* skip) {
+    *skip = false;
     if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
     if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
     if (N > 0) {
@@ -263,7 +283,10 @@ kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* impor
             return fail(KMD_ERR_DIM, "halo (%d,%d) smaller than required (%d,%d) for r_max=%d", halo_top,
                         halo_bot, need_top, need_bot, r);
     }
-    if (N == 0) return KMD_OK;
+    if (N == 0) {
+        *skip = true;
+        return KMD_OK;
+    }
     if (!radiance || !importance || !out) return fail(KMD_ERR_NULL, "radiance/importance/out is NULL");
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
     const int buf_rows = halo_top + band_rows + halo_bot;
@@ -273,10 +296,76 @@ kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* impor
         overlaps(out, 3 * N * oplane, importance, M * N * bplane) ||
         (M > 1 && overlaps(out, 3 * N * oplane, blend, M * N * oplane)))
         return fail(KMD_ERR_ALIAS, "out overlaps an input");
+    kmd::FusedParams q{};
+    q.rad = radiance; q.imp = importance; q.blend = blend; q.out = out;
+    q.N = N; q.W = W; q.H = H_global;
+    q.row_base = y0 - halo_top; q.buf_rows = buf_rows; q.out_y0 = y0; q.out_rows = band_rows;
+    *p = q;
+    return KMD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kmd_status kmd_decode_filter_fuse_band(const float* radiance, const float* importance,
+                                       const float* blend, float* out, int32_t N,
+                                       int32_t band_rows, int32_t W, int32_t halo_top,
+                                       int32_t halo_bot, int32_t y0, int32_t H_global,
+                                       const kmd_config* cfg, kmd_stream_t stream) {
+    return kmd_decode_filter_fuse_band_part(radiance, importance, blend, out, N, band_rows, W, halo_top, halo_bot,
+                                            y0, H_global, cfg, KMD_BAND_ALL, stream);
+}
+
+kmd_status kmd_decode_filter_fuse_band_part(const float* radiance, const float* importance,
+                                            const float* blend, float* out, int32_t N,
+                                            int32_t band_rows, int32_t W, int32_t halo_top,
+                                            int32_t halo_bot, int32_t y0, int32_t H_global,
+                                            const kmd_config* cfg, int32_t part, kmd_stream_t stream) {
+    g_err[0] = 0;
+    if (part != KMD_BAND_ALL && part != KMD_BAND_INTERIOR && part != KMD_BAND_SEAMS)
+        return fail(KMD_ERR_CONFIG, "part=%d not one of KMD_BAND_ALL/INTERIOR/SEAMS", part);
     kmd::FusedParams p{};
-    p.rad = radiance; p.imp = importance; p.blend = blend; p.out = out;
-    p.N = N; p.W = W; p.H = H_global;
-    p.row_base = y0 - halo_top; p.buf_rows = buf_rows; p.out_y0 = y0; p.out_rows = band_rows;
+    bool skip = false;
+    kmd_status s = band_params(radiance, importance, blend, out, N, band_rows, W, halo_top, halo_bot, y0, H_global,
+                               cfg, &p, &skip);
+    if (s || skip) return s;
+    if (part == KMD_BAND_ALL) return run_fused(p, cfg, (cudaStream_t)stream);
+    // Interior / seam split on the TMA kernel's global tile grid: a tile row
+    // is interior when every row its windows read is an owned row (or is
+    // clamped at a frame edge that has no neighbour), so it can run before the
+    // halo rows arrive; the seam tile rows are the rest.  Each tile is
+    // computed once, by one of the two launches, in the same order as in the
+    // whole-frame call (bitwise equal results).
+    {
+        kmd::FusedParams t = p;
+        t.M = cfg->num_sizes;
+        for (int i = 0; i < KMD_MAX_SIZES; ++i) t.sizes[i] = i < cfg->num_sizes ? cfg->sizes[i] : 1;
+        if (!kmd::tma_supported(t))  // other kernels: no split, the seam part does the whole band
+            return part == KMD_BAND_SEAMS ? run_fused(p, cfg, (cudaStream_t)stream) : KMD_OK;
+    }
+    const int TH = kmd::tma_tile_rows(), r = rmax_of(cfg);
+    const int tile_begin = (y0 / TH) * TH;
+    const int tiles_y = (y0 + band_rows - tile_begin + TH - 1) / TH;
+    int k_lo = 0, k_hi = tiles_y;
+    if (halo_top > 0)
+        while (k_lo < tiles_y && tile_begin + k_lo * TH - r < y0) ++k_lo;
+    if (halo_bot > 0)
+        while (k_hi > 0 && tile_begin + (k_hi - 1) * TH + TH + r > y0 + band_rows) --k_hi;
+    if (k_hi < k_lo) k_hi = k_lo;  // no interior tile row
+    if (part == KMD_BAND_INTERIOR) {
+        if (k_hi == k_lo) return KMD_OK;
+        p.tile_y_begin = tile_begin + k_lo * TH;
+        p.tile_rows_a = k_hi - k_lo;
+        p.tile_rows_total = k_hi - k_lo;
+    } else {
+        const int total = k_lo + (tiles_y - k_hi);
+        if (total == 0) return KMD_OK;
+        p.tile_y_begin = tile_begin;
+        p.tile_rows_a = k_lo;
+        p.tile_y_begin_b = tile_begin + k_hi * TH;
+        p.tile_rows_total = total;
+    }
     return run_fused(p, cfg, (cudaStream_t)stream);
 }
 

@@ -24,6 +24,14 @@ struct FusedParams {
     int out_y0;          // global row of out/blend row 0
     int out_rows;        // rows of out/blend
     int tile_y_begin;    // global row of the first tile (multiple of the tile height)
+    // tile rows of a launch: tile_rows_a rows from tile_y_begin, then (if the
+    // launch has more) rows from tile_y_begin_b -- the band interior / seam
+    // split (kmd_band.cu); tile_rows_a = INT_MAX for one contiguous range
+    int tile_rows_a;
+    int tile_y_begin_b;
+    // > 0: the tile rows of this launch (else every tile row of the output);
+    // set together with tile_y_begin / tile_rows_a / tile_y_begin_b
+    int tile_rows_total;
     int M;               // number of maps / sizes
     int rmax;            // max_i (k_i - 1)/2
     int blend_is_logits;
@@ -116,4 +124,62 @@ __device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ~2 ulp
     return y;
 }
 
+}  // namespace kmd
+
+// ---- tcgen05 tensor memory (TMEM) as per-thread staging ---------------------
+// The TMA kernel keeps each field thread's radiance column in TMEM (lane =
+// the thread's lane within its warp's quadrant, one 32-bit column per value):
+// it is loaded from shared memory once per tile and read back by every size's
+// field job, instead of 3 shared-memory loads per field pixel per size.
+namespace kmd {
+__device__ __forceinline__ void tmem_alloc(unsigned* smem_dst, unsigned ncols) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(unsigned taddr, unsigned ncols) {  // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before_sync() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after_sync() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 16 consecutive 32-bit columns of this thread's lane
+__device__ __forceinline__ void tmem_st16(unsigned taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 4 consecutive columns; the registers are valid only after tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld4(unsigned taddr, float4& v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// after tmem_wait_ld(): makes every later use of v depend on the wait (the
+// compiler cannot hoist a use of a tcgen05.ld result above the wait)
+__device__ __forceinline__ void tmem_reg_fence(float4& v) {
+    asm volatile("" : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w));
+}
+}  // namespace kmd
+namespace kmd {
+// columns c, c+1, c+2 of this thread's lane into v.x, v.y, v.z (v.w untouched);
+// valid only after tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld3(unsigned taddr, float4& v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                 : "=f"(v.x), "=f"(v.y)
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(v.z) : "r"(taddr + 2) : "memory");
+}
+__device__ __forceinline__ void tmem_reg_fence3(float4& v) { asm volatile("" : "+f"(v.x), "+f"(v.y), "+f"(v.z)); }
 }  // namespace kmd

@@ -5,6 +5,8 @@
 // Used by the forward kernel (kmd_tma.cu) and the tiled backward (kmd_bwd.cu).
 #pragma once
 
+#include <type_traits>
+
 #include "kmd_common.cuh"
 
 namespace kmd {
@@ -49,10 +51,18 @@ __device__ __forceinline__ void gw_line(F&& field, E&& emit) {
     gw_block<R, N, 0>(suf, field, emit);
 }
 
+// Field values base .. base+CNT-1 into dst: f1(j) one value at a time, or,
+// when f1 takes (std::integral_constant<int, CNT>, float4* dst, int base), the
+// whole block in one call (the TMA kernel's field: TMEM loads issued together,
+// one wait).
 template <int CNT, class F1>
 __device__ __forceinline__ void fill_field(float4* dst, int base, F1& f1) {
+    if constexpr (std::is_invocable_v<F1&, std::integral_constant<int, CNT>, float4*, int>) {
+        f1(std::integral_constant<int, CNT>{}, dst, base);
+    } else {
 #pragma unroll
-    for (int t = 0; t < CNT; ++t) dst[t] = f1(base + t);
+        for (int t = 0; t < CNT; ++t) dst[t] = f1(base + t);
+    }
 }
 
 // The vertical (field-warp) Gil-Werman line: same sums in the same order as

@@ -14,6 +14,7 @@ cudaError_t launch_fused_ws(FusedParams p, cudaStream_t stream);
 // v3: persistent warp-specialised kernel fed by TMA, k <= 13, W % 4 == 0 (kmd_tma.cu)
 bool tma_supported(const FusedParams& p);
 cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream);
+int tma_tile_rows();  // output rows per TMA-kernel tile (the global tile grid's pitch)
 
 // fusion only, Eq. 5 (kmd_fuse.cu)
 cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
@@ -48,6 +49,10 @@ cudaError_t launch_temporal(const float* cur_rad, const float* prev_rad, const f
                             const float* prev_nrm, const unsigned char* prev_valid, const float* cur_pos,
                             const float* cur_nrm, const float* motion, float* accum, unsigned char* mask, int N,
                             int H, int W, float pos_tol, float normal_tol, float alpha, cudaStream_t st);
+
+// error detail for kmd_last_error() from any translation unit (kmd_api.cu)
+kmd_status api_fail(kmd_status s, const char* fmt, ...);
+void api_clear_error();
 
 // kernel variant of the last fused launch on this host thread (kmd_last_kernel)
 enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_BWD_TILE = 10, LK_BWD_TMA = 11, LK_TMA_SPEC = 100,

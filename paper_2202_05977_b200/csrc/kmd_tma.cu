@@ -41,10 +41,21 @@
 namespace kmd {
 namespace tma {
 
+// development switches (role isolation / ablation probes, env KMD_DEBUG): only
+// in builds with -DKMD_DEBUG_SWITCHES, compiled out of the production kernel
+#ifdef KMD_DEBUG_SWITCHES
+#define KMD_DBG(bit) (p.debug & (bit))
+#else
+#define KMD_DBG(bit) 0
+#endif
+
 #ifdef KMD_SPIN_WAIT
 #define mbar_wait mbar_spin
 #endif
 
+#ifndef KMD_SEG
+#define KMD_SEG 7                   // fusion segment length (see seg_start below)
+#endif
 constexpr int RMAX = 6;
 constexpr int TW = 52;              // output columns per tile
 constexpr int FW = TW + 2 * RMAX;   // 64 field columns (2 warps), global x0-6 .. x0+57
@@ -58,14 +69,53 @@ constexpr int FH = TH + 2 * RMAX;   // 39 field rows in every box
 // multiple of 16 bytes when it is negative (measured on this B200: -6 faults,
 // -8 works), and 68 columns cover x0-6 .. x0+57 (and the 52 output columns).
 constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
-constexpr int BW = 68;              // box width (== V stride; 4 mod 8 -> conflict-free fusion reads)
-constexpr int VS = 68;
-constexpr int SEG = 7;              // pixels per fusion thread (segments of 7 or 6 pixels)
-constexpr int NSEG = 8;             // segments per output row: 52 = 4 x 7 + 4 x 6
-constexpr int NI = TH > 24 ? 3 : 4; // input (importance) ring depth
+constexpr int BW = 68;              // box width
+// V row stride (float4s): SEG 7 reads a row's 8 segments per quarter warp, so
+// any stride is conflict-free (64: no padding); SEG 9 / 13 need 70 / 68
+constexpr int VS = KMD_SEG == 9 ? 70 : KMD_SEG == 13 ? 68 : 64;
+// Fusion segments: a fusion thread owns SEG consecutive output pixels of one
+// tile row (NSEG segments per row).  Segment starts are distinct mod 8 (and,
+// with the V row stride VS below, any 8 consecutive fusion threads start in 8
+// distinct 16-byte bank groups), so every LDS.128 of V is conflict-free.
+//   SEG 7 : 8 segments 0,6,12,19,26,33,39,45 (lengths 6,6,7,7,7,6,6,7), rows by KMD_ROWMAP
+//   SEG 9 : 6 segments 0,9,18,27,36,45 (the last 7 long), VS = 70 (= 6 mod 8)
+//   SEG 13: 4 segments 0,13,26,39, VS = 68
+constexpr int SEG = KMD_SEG;
+static_assert(SEG == 7 || SEG == 9 || SEG == 13, "fusion segment layouts: 7, 9 or 13 pixels");
+constexpr int NSEG = SEG == 7 ? 8 : SEG == 9 ? 6 : 4;   // segments per output row
+__host__ __device__ constexpr int seg_start(int sub) {
+    return SEG == 7 ? (int)((0x2d27211a130c0600ull >> (8 * sub)) & 0xff) : sub * SEG;
+}
+__host__ __device__ constexpr int seg_len(int sub) {
+    return SEG == 7 ? (int)((0x76677766u >> (4 * sub)) & 0xf) : (sub == NSEG - 1 ? TW - sub * SEG : SEG);
+}
+// Radiance in tensor memory (KMD_TMEM_RAD 1): each field warp copies its
+// 32 radiance columns of the tile from the (single) shared-memory box into its
+// TMEM quadrant once per tile and its size jobs read them back with tcgen05.ld;
+// the freed box buys the fourth V slot.  0: every job reads the radiance from
+// a double-buffered shared-memory box.
+#ifndef KMD_TMEM_RAD
+#define KMD_TMEM_RAD 1
+#endif
+constexpr bool TMEM_RAD = KMD_TMEM_RAD;
+constexpr int NRAD = TMEM_RAD ? 1 : 2;  // radiance boxes in shared memory
+#ifndef KMD_NI
+#define KMD_NI 3
+#endif
+#ifndef KMD_NV
+#define KMD_NV (KMD_TMEM_RAD ? 4 : 3)
+#endif
+constexpr int NI = KMD_NI;          // input (importance) ring depth
 constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
-constexpr int NV = 3;               // V ring depth (field -> fusion)
-constexpr int NFIELD = 4;           // field warps
+constexpr int NV = KMD_NV;          // V ring depth (field -> fusion)
+constexpr unsigned TMEM_COLS = 256; // 4 columns (r, g, b, -) per box row: 4 x 39 <= 256
+// field warps; a field job is one (tile, size, 32-column half) walk, and the
+// jobs of consecutive tiles are dealt to the field warps round-robin in one
+// global sequence, so any NFIELD keeps every warp equally loaded
+#ifndef KMD_NFIELD
+#define KMD_NFIELD 4
+#endif
+constexpr int NFIELD = KMD_NFIELD;
 constexpr int NFUSE = (TH * NSEG + 31) / 32;  // fusion warps (one thread per (row, segment))
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 // Warp -> role: 0 = producer, field, fusion in ascending warp ids (default);
@@ -93,12 +143,22 @@ constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to f
 #ifndef KMD_ROWMAP
 #define KMD_ROWMAP 1
 #endif
-constexpr bool ROWMAP = KMD_ROWMAP && TH == 27;
+constexpr bool ROWMAP = KMD_ROWMAP && TH == 27 && KMD_SEG == 7;
 // output row of fusion thread c (0 .. 32 NFUSE - 1; its segment is c % NSEG);
 // rows >= TH are idle lanes
 __host__ __device__ constexpr int fuse_row(int c) {
     return ROWMAP ? ((c >> 5) < 6 ? 8 * (c >> 6) + ((c >> 5) & 1) + 2 * ((c >> 3) & 3) : 24 + ((c >> 3) & 3))
                   : c / NSEG;
+}
+__host__ __device__ constexpr int fuse_seg_of(int c) { return c % NSEG; }
+// segments tile each row exactly (starts increasing, lengths summing to TW)
+constexpr bool segs_tile_row() {
+    int x = 0;
+    for (int sub = 0; sub < NSEG; ++sub) {
+        if (seg_start(sub) != x || seg_len(sub) < 1 || seg_len(sub) > SEG) return false;
+        x += seg_len(sub);
+    }
+    return x == TW;
 }
 // every (row, segment) of the tile has exactly one fusion thread
 constexpr bool fuse_map_is_bijective() {
@@ -106,19 +166,19 @@ constexpr bool fuse_map_is_bijective() {
     for (int c = 0; c < 32 * ((TH * NSEG + 31) / 32); ++c) {
         const int r = fuse_row(c);
         if (r >= TH) continue;
-        if (segs[r] & (1u << (c % NSEG))) return false;
-        segs[r] |= 1u << (c % NSEG);
+        if (segs[r] & (1u << fuse_seg_of(c))) return false;
+        segs[r] |= 1u << fuse_seg_of(c);
     }
     for (int r = 0; r < TH; ++r)
         if (segs[r] != (1u << NSEG) - 1) return false;
     return true;
 }
-static_assert(TH <= 32 && fuse_map_is_bijective(), "fusion thread map covers each tile row with 8 segments");
+static_assert(TH <= 32 && fuse_map_is_bijective() && segs_tile_row(), "fusion thread map covers each tile row once");
 template <bool IN16>
 struct InElem {
     using T = float;
     static constexpr int IW = BW;
-    static constexpr int BBW = ROWMAP ? 60 : 56;  // blend box width (multiple of 4: 16-byte TMA rows)
+    static constexpr int BBW = ROWMAP ? 60 : SEG == 13 ? 52 : 56;  // blend box width (multiple of 4: 16-byte TMA rows)
 };
 template <>
 struct InElem<true> {
@@ -156,13 +216,14 @@ struct RadBuf {
 };
 template <bool IN16>
 struct SmemT {
-    RadBuf rad[2];
+    RadBuf rad[NRAD];
     InSlotT<IN16> in[NI];
     Slot slot[NV];
     BSlotT<IN16> bl[NB];
     float stage[3][TH][TW];
-    unsigned long long rad_full[2], rad_empty[2], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV], b_full[NB],
-        b_empty[NB];
+    unsigned long long rad_full[NRAD], rad_empty[NRAD], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV],
+        b_full[NB], b_empty[NB];
+    unsigned tmem_base;                // TMEM address of the allocation (TMEM_RAD)
 };
 using Smem = SmemT<false>;
 static_assert(sizeof(SmemT<false>) <= 232448 && sizeof(SmemT<true>) <= 232448, "227 KB of shared memory per CTA");
@@ -233,54 +294,105 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
     const int r = t - c.n * per_frame;
     const int ty = r / tiles_x;
     c.x0 = (r - ty * tiles_x) * TW;
-    c.y0 = p.tile_y_begin + ty * TH;
+    c.y0 = ty < p.tile_rows_a ? p.tile_y_begin + ty * TH : p.tile_y_begin_b + (ty - p.tile_rows_a) * TH;
     return c;
-}
-
-// rows of the box (global y0-6 .. y0+32) outside the frame/buffer take the
-// value of the nearest valid row (clamp-to-edge, reading R1)
-template <int STRIDE = BW, class T>
-__device__ __forceinline__ void fix_rows(T* col, int plane_stride, int nplanes, int top, int bot) {
-    for (int pl = 0; pl < nplanes; ++pl) {
-        T* c = col + pl * plane_stride;
-        if (top > 0) {
-            const T v = c[top * STRIDE];
-            for (int r = 0; r < top; ++r) c[r * STRIDE] = v;
-        }
-        if (bot < FH) {
-            const T v = c[(bot - 1) * STRIDE];
-            for (int r = bot; r < FH; ++r) c[r * STRIDE] = v;
-        }
-    }
 }
 
 // ------------------------------------------------------------ field warps
 // cc: the thread's field column in the radiance box; ci: the same column in
-// the importance box (they differ by the bf16 box alignment shift, see xa)
-template <int R, class SM, class IS>
-__device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci) {
+// the importance box (they differ by the bf16 box alignment shift, see xalign).
+// Clamp-to-edge rows (reading R1): box rows outside the frame / buffer
+// [top, bot) read the nearest valid row.  Only border tiles take the CLAMP
+// variant (for the importance box; the radiance rows are clamped when they are
+// copied to TMEM); the boxes in shared memory are never written by the
+// generic proxy.  tm: this warp's TMEM quadrant (TMEM_RAD), box row f's
+// (r, g, b) at columns 4f .. 4f+2.
+template <int R, bool CLAMP, class SM, class IS>
+__device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci, int top,
+                                          int bot, unsigned tm) {
     constexpr int IW = sizeof(in.I[0]) / sizeof(in.I[0][0]);
     const int c = h * 32 + (threadIdx.x & 31);
-    const auto* Ib = &in.I[RMAX - R][ci];
-    const float* Rb = &sm.rad[rb].v[0][RMAX - R][cc];
+    const auto* Ib = &in.I[0][ci];
+    const float* Rb = &sm.rad[rb].v[0][0][cc];
     float4* Vc = &sl.V[0][c];
-    gw_line_field<R, TH>(
-        [&](int f) {
-            const float v = ld_in(Ib + f * IW);
-            const float r = Rb[f * BW], g = Rb[FH * BW + f * BW], b = Rb[2 * FH * BW + f * BW];
-            const float e = exp_acc(v);  // once per field pixel (Eq. 3's shared weight)
-            const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(g, b));  // pairs (e, er), (eg, eb)
-            return make_float4(e, e * r, gb.x, gb.y);
-        },
-        [&](int oy, float4 v) {
-            // two 8-byte stores keep the FADD2 register pairs in place (no MOVs
-            // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
-            // (one STS.128 would halve the store wavefronts but costs MOVs to
-            // assemble the quad: measured 7% slower)
-            const unsigned a = smem_u32(&Vc[oy * VS]);
-            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
-            asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
-        });
+    auto emit = [&](int oy, float4 v) {
+        // two 8-byte stores keep the FADD2 register pairs in place (no MOVs
+        // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
+        // (one STS.128 would halve the store wavefronts but costs MOVs to
+        // assemble the quad: measured 7% slower)
+        const unsigned a = smem_u32(&Vc[oy * VS]);
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+        asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
+    };
+    if constexpr (TMEM_RAD) {
+        // one block of field rows: the TMEM loads of the block issued together,
+        // one wait, then e = exp(I) and the premultiplied quad per row
+        gw_line_field<R, TH>(
+            [&](auto cnt, float4* dst, int base) {
+                constexpr int CNT = decltype(cnt)::value;
+#pragma unroll
+                for (int t = 0; t < CNT; ++t) {
+                    const int row = RMAX - R + base + t;
+                    tmem_ld3(tm + 4 * row, dst[t]);  // (r, g, b) -> .x .y .z
+                    // e = exp(I) once per field pixel (Eq. 3's shared weight), in .w
+                    // while the TMEM loads are in flight
+                    dst[t].w = exp_acc(ld_in(Ib + (CLAMP ? clampi(row, top, bot - 1) : row) * IW));
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int t = 0; t < CNT; ++t) {
+                    tmem_reg_fence3(dst[t]);
+                    const float e = dst[t].w;
+                    const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(dst[t].y, dst[t].z));
+                    dst[t] = make_float4(e, e * dst[t].x, gb.x, gb.y);
+                }
+            },
+            emit);
+    } else {
+        gw_line_field<R, TH>(
+            [&](int f) {
+                const int row = CLAMP ? clampi(RMAX - R + f, top, bot - 1) : RMAX - R + f;
+                const float v = ld_in(Ib + row * IW);
+                const float r = Rb[row * BW], g = Rb[FH * BW + row * BW], b = Rb[2 * FH * BW + row * BW];
+                const float e = exp_acc(v);  // once per field pixel (Eq. 3's shared weight)
+                const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(g, b));  // pairs (e, er), (eg, eb)
+                return make_float4(e, e * r, gb.x, gb.y);
+            },
+            emit);
+    }
+}
+
+// This warp's radiance columns of the tile (rows clamped, reading R1) from the
+// shared-memory box into its TMEM quadrant: 16 columns (4 box rows) per store.
+__device__ __forceinline__ void rad_to_tmem(const RadBuf& rad, int cc, int top, int bot, unsigned tm) {
+#pragma unroll 1
+    for (int f0 = 0; f0 < FH; f0 += 4) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int row = clampi(f0 + k, top, bot - 1);
+            v[4 * k + 0] = rad.v[0][row][cc];
+            v[4 * k + 1] = rad.v[1][row][cc];
+            v[4 * k + 2] = rad.v[2][row][cc];
+            v[4 * k + 3] = 0.f;
+        }
+        tmem_st16(tm + 4 * f0, v);
+    }
+    tmem_wait_st();
+}
+
+template <bool CLAMP, class SM, class IS>
+__device__ __forceinline__ void field_dispatch(int R, SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci,
+                                               int top, int bot, unsigned tm) {
+    switch (R) {
+        case 0: field_job<0, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 1: field_job<1, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 2: field_job<2, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 3: field_job<3, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 4: field_job<4, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 5: field_job<5, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        default: field_job<6, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+    }
 }
 
 // --------------------------------------------------------------- fusion warps
@@ -443,6 +555,9 @@ struct Spec {
 };
 
 // --------------------------------------------------------------------- kernel
+// Registers: the register file is split over the 4 SM sub-partitions (warp w
+// on wid % 4), so the budget is 16384 / (32 x the warps of the busiest one);
+// ptxas derives it from the launch bounds (12 warps -> 168, 13-16 -> 128).
 template <class SP>
 __global__ void __launch_bounds__(NTHREADS, 1)
     fused_tma_kernel(const __grid_constant__ FusedParams p, const __grid_constant__ CUtensorMap tm_rad,
@@ -453,14 +568,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     SmemK& sm = *reinterpret_cast<SmemK*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = SP::M > 0 ? SP::M : p.M;
-    const bool has_blend = p.blend != nullptr && !(p.debug & 16);
+    const bool has_blend = p.blend != nullptr && !(KMD_DBG(16));
     unsigned rpack = 0;  // radius of size i in bits 4i..4i+3
     for (int i = 0; i < M; ++i) rpack |= (unsigned)((p.sizes[i] - 1) / 2) << (4 * i);
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NRAD; ++b) {
             mbar_init(&sm.rad_full[b], 1);
-            mbar_init(&sm.rad_empty[b], NFIELD);
+            mbar_init(&sm.rad_empty[b], NFIELD);       // every field warp, once per tile
         }
         for (int s = 0; s < NI; ++s) {
             mbar_init(&sm.in_full[s], 1);
@@ -476,7 +591,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (TMEM_RAD && warp == TMA_WARP) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+    if constexpr (VS > 64) {
+        // V columns past the 64 field columns: read (not stored) by the last
+        // segment's recomputed pixels; keep them finite
+        constexpr int PADC = VS - 64;
+        for (int k = threadIdx.x; k < NV * TH * PADC; k += NTHREADS)
+            sm.slot[k / (TH * PADC)].V[(k / PADC) % TH][64 + k % PADC] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (TMEM_RAD) tmem_fence_before_sync();
     __syncthreads();
+    if (TMEM_RAD) tmem_fence_after_sync();
     const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 #ifdef KMD_INSTR
     unsigned long long instr[INSTR_TAGS] = {};
@@ -486,7 +611,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == TMA_WARP) {
         // ------------------------------------------------------------- TMA
         if (lane == 0) {
-            if (!(p.debug & 8)) {
+            if (!(KMD_DBG(8))) {
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_rad)) : "memory");
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
@@ -500,9 +625,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // and the rings are NI, NB >= NV + 1 deep).
             for (int tl = 0; tl < my_tiles; ++tl) {
                 const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
-                const int rb = tl & 1;
-                IWAIT(0, mbar_wait(&sm.rad_empty[rb], ((tl >> 1) & 1) ^ 1));
-                if (p.debug & 256) {
+                const int rb = tl % NRAD;
+                IWAIT(0, mbar_wait(&sm.rad_empty[rb], ((tl / NRAD) & 1) ^ 1));
+                if (KMD_DBG(256)) {
                     mbar_arrive(&sm.rad_full[rb]);
                 } else {
                     mbar_arrive_expect_tx(&sm.rad_full[rb], RAD_BYTES);
@@ -512,7 +637,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int i = 0; i < M; ++i) {
                     const int seq = tl * M + i, s = seq % NI;
                     IWAIT(1, mbar_wait(&sm.in_empty[s], ((seq / NI) & 1) ^ 1));
-                    if (p.debug & 128) {
+                    if (KMD_DBG(128)) {
                         mbar_arrive(&sm.in_full[s]);
                     } else {
                         mbar_arrive_expect_tx(&sm.in_full[s], I_BYTES);
@@ -531,32 +656,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp >= FIELD_W0 && warp < FIELD_W0 + NFIELD) {
         // ----------------------------------------------------------- field
+        // Jobs (tile tl, size i, 32-column half h) in one global sequence
+        // g = (tl * M + i) * 2 + h, dealt round-robin to the field warps (NFIELD
+        // even: a warp always takes the same half).  Every field warp passes
+        // every tile's radiance once, in order: waits for the box, (TMEM_RAD)
+        // copies its half's columns to its TMEM quadrant and releases the box,
+        // then runs its jobs of the tile.  A job waits for a free V slot and
+        // its importance box, writes the vertical sums of its 32 columns and
+        // releases the importance slot and the V slot (to the fusion warps).
+        static_assert(NFIELD % 2 == 0, "field warps keep one column half each");
         const int fw = warp - FIELD_W0;
+        const int h = fw & 1;
         const int ylo = max(0, p.row_base), yhi = min(p.H, p.row_base + p.buf_rows) - 1;
+        const unsigned tm = TMEM_RAD ? sm.tmem_base + ((unsigned)(32 * (warp & 3)) << 16) : 0u;
+        const int c = h * 32 + lane;
+        int g = fw;
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
-            const int rb = tl & 1;
+            const int rb = tl % NRAD;
             const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
             const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
-            const bool border_rows = top > 0 || bot < FH;
-            IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl >> 1) & 1));
-            // one (size i, 32-column half h) job: wait for its importance box and a
-            // free V slot, replicate border rows, vertical box sums, release
-            auto job = [&](int i, int h, auto&& body) {
-                const int seq = tl * M + i, si = seq % NI, sv = seq % NV;
-                const int c = h * 32 + lane;
-                const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
-                const int ci = cc + xalign<SP::IN16>(tc.x0);
+            const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
+            const int ci = cc + xalign<SP::IN16>(tc.x0);
+            IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl / NRAD) & 1));
+            if constexpr (TMEM_RAD) {
+                rad_to_tmem(sm.rad[0], cc, top, bot, tm);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.rad_empty[0]);
+            }
+#pragma unroll 1
+            for (; g < 2 * M * (tl + 1); g += NFIELD) {
+                const int seq = g >> 1, i = seq - tl * M;
+                const int si = seq % NI, sv = seq % NV;
                 Slot& sl = sm.slot[sv];
                 auto& in = sm.in[si];
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
                 IWAIT(4, mbar_wait(&sm.in_full[si], (seq / NI) & 1));
-                if (border_rows && !(p.debug & 4)) {
-                    fix_rows<InElem<SP::IN16>::IW>(&in.I[0][ci], FH * BW, 1, top, bot);
-                    fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
-                    fence_proxy_async();  // generic writes before the next TMA overwrite
-                }
-                if (!(p.debug & 32)) body(in, sl, cc, ci);
+                const int R = (rpack >> (4 * i)) & 15;
+                if (top > 0 || bot < FH) field_dispatch<true>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                else field_dispatch<false>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
                 // one arrive per warp: __syncwarp orders every lane's shared
                 // memory accesses before the elected lane's release-arrive
                 __syncwarp();
@@ -564,40 +702,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_arrive(&sm.in_empty[si]);
                     mbar_arrive(&sm.v_full[sv]);
                 }
-            };
-            {
-#pragma unroll 1
-                for (int jl = fw; jl < 2 * M; jl += NFIELD) {
-                    const int i = jl >> 1, h = jl & 1;
-                    job(i, h, [&](const auto& in, Slot& sl, int cc, int ci) {
-                        switch ((rpack >> (4 * i)) & 15) {
-                            case 0: field_job<0>(sm, in, sl, rb, h, cc, ci); break;
-                            case 1: field_job<1>(sm, in, sl, rb, h, cc, ci); break;
-                            case 2: field_job<2>(sm, in, sl, rb, h, cc, ci); break;
-                            case 3: field_job<3>(sm, in, sl, rb, h, cc, ci); break;
-                            case 4: field_job<4>(sm, in, sl, rb, h, cc, ci); break;
-                            case 5: field_job<5>(sm, in, sl, rb, h, cc, ci); break;
-                            default: field_job<6>(sm, in, sl, rb, h, cc, ci); break;
-                        }
-                    });
-                }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.rad_empty[rb]);
+            if constexpr (!TMEM_RAD) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.rad_empty[rb]);
+            }
         }
     } else {
         // ----------------------------------------------------------- fusion
         const int c = threadIdx.x - FUSE_W0 * 32;
-        // thread = (row, segment); segments start at 0,6,12,19,26,33,39,45
-        // (lengths 6,6,7,7,7,6,6,7): the starts are distinct mod 8, so the 8
-        // lanes of a row hit 8 different 16-byte bank groups with every
-        // LDS.128 of V.  Every thread computes 7 pixels (the 7th of a 6-pixel
-        // segment is recomputed by its neighbour and not stored).
-        const int sub = c % NSEG;
+        // thread = (row, segment), see seg_start / seg_len.  Every thread
+        // computes SEG pixels; the pixels of a shorter segment past its length
+        // are recomputed by the neighbour (or lie past the tile) and not stored.
+        const int sub = fuse_seg_of(c);
         const int ty = fuse_row(c);
         const bool active = ty < TH;  // the last fusion warp may have spare lanes
-        const int xs = (0x2d27211a130c0600ull >> (8 * sub)) & 0xff;
-        const int len = (0x76677766u >> (4 * sub)) & 0xf;
+        const int xs = seg_start(sub);
+        const int len = seg_len(sub);
         int vs = 0, vph = 0, bs = 0, bph = 0;  // V / blend ring slot and phase of the current step
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
@@ -695,7 +816,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     fence_proxy_async();
                     fuse_bar();
                     // one TMA store of the pair of planes [2][27][52] (clipped at the frame edge)
-                    if (c == 0 && !(p.debug & 1))
+                    if (c == 0 && !(KMD_DBG(1)))
                         tma_store_3d(&tm_out, tc.x0, tc.y0, 2 * (tc.n * M + i), &sm.stage[0][0][0]);
                     if (++vs == NV) { vs = 0; vph ^= 1; }
                     if (++bs == NB) { bs = 0; bph ^= 1; }
@@ -734,7 +855,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < M; ++i) {
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                if (!(p.debug & 64) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
+                if (!(KMD_DBG(64)) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
                                                                    (rpack >> (4 * i)) & 15);
                 __syncwarp();
                 if ((c & 31) == 0) {
@@ -745,7 +866,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (++vs == NV) { vs = 0; vph ^= 1; }
                 if (++bs == NB) { bs = 0; bph ^= 1; }
             }
-            if (p.debug & 1024) continue;
+            if (KMD_DBG(1024)) continue;
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
             if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
             IWAIT(9, fuse_bar());
@@ -768,7 +889,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             // rare: pixels outside the unshifted exp range -> exact evaluation
-            if (bad && row_ok && active && !(p.debug & 2)) {
+            if (bad && row_ok && active && !(KMD_DBG(2))) {
                 for (int j = 0; j < len; ++j) {
                     const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
@@ -799,7 +920,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // TMA store; it clips the parts beyond W / out_rows.  (A TMA store
                 // with a negative coordinate faults on this B200, so the first tile
                 // of a row band that starts inside a tile is stored by hand below.)
-                if (c == 0 && !(p.debug & 1)) tma_store_3d(&tm_out, tc.x0, tc.y0 - p.out_y0, tc.n * 3, &sm.stage[0][0][0]);
+                if (c == 0 && !(KMD_DBG(1))) tma_store_3d(&tm_out, tc.x0, tc.y0 - p.out_y0, tc.n * 3, &sm.stage[0][0][0]);
             } else {
                 float* out = p.out + (size_t)tc.n * 3 * ((size_t)p.out_rows * p.W);
                 for (int idx = c; idx < 3 * TH * TW; idx += NFUSE * 32) {
@@ -812,6 +933,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         }
         if (c == 0) bulk_wait0();
+    }
+    if constexpr (TMEM_RAD) {
+        // every field warp's TMEM traffic is complete before the deallocation
+        tmem_fence_before_sync();
+        __syncthreads();
+        if (warp == TMA_WARP) {
+            tmem_fence_after_sync();
+            tmem_dealloc(sm.tmem_base, TMEM_COLS);
+        }
     }
 #ifdef KMD_INSTR
     instr[15] = (unsigned long long)(clock64() - t_begin);
@@ -863,9 +993,12 @@ extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
 
 // backward pass A (NEXT row 3, kmd_bwd_tma.cu): whole frames only; the pairs
 // (a_i / den_i, G.R_i) go to ws as [N*M][2][H][W]
+int tma_tile_rows() { return tma::TH; }
+
 cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream) {
     using namespace tma;
     p.tile_y_begin = 0;
+    p.tile_rows_a = 0x7fffffff;
     const int tiles_y = (p.H + TH - 1) / TH, tiles_x = (p.W + TW - 1) / TW;
     const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
     if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
@@ -904,8 +1037,14 @@ bool tma_supported(const FusedParams& p) {
 
 cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     using namespace tma;
-    p.tile_y_begin = (p.out_y0 / TH) * TH;
-    const int tiles_y = (p.out_y0 + p.out_rows - p.tile_y_begin + TH - 1) / TH;
+    int tiles_y;
+    if (p.tile_rows_total > 0) {
+        tiles_y = p.tile_rows_total;  // explicit tile rows (band interior / seams)
+    } else {
+        p.tile_y_begin = (p.out_y0 / TH) * TH;
+        p.tile_rows_a = 0x7fffffff;
+        tiles_y = (p.out_y0 + p.out_rows - p.tile_y_begin + TH - 1) / TH;
+    }
     const int tiles_x = (p.W + TW - 1) / TW;
     const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
     if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
@@ -949,7 +1088,7 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
         if (softmax && !alb && p.M == 6) return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 6, true>>, LK_TMA_BF16 + 6);
         return spec(fused_tma_kernel<Runtime16>, LK_TMA_BF16);
     }
-    if (!(p.debug & 2048)) {
+    if (!(KMD_DBG(2048))) {
         if (softmax && !alb) switch (p.M) {
                 case 2: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>, LK_TMA_SPEC + 2);
                 case 3: return spec(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 3>>, LK_TMA_SPEC + 3);

@@ -72,7 +72,9 @@ EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_bf16", "kmd_decode_
            "kmd_combine_resolutions", "kmd_backward_workspace_bytes",
            "kmd_decode_filter_fuse_backward", "kmd_temporal_accumulate",
            "kmd_remodulate", "kmd_decode_filter", "kmd_fuse",
-           "kmd_decode_filter_fuse_band", "kmd_host_workspace_bytes",
+           "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_band_part", "kmd_nccl_unique_id",
+           "kmd_comm_init", "kmd_comm_destroy", "kmd_halo_exchange", "kmd_band_step",
+           "kmd_host_workspace_bytes",
            "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
            "kmd_status_string", "kmd_last_error", "kmd_version", "kmd_last_kernel")
 
@@ -109,6 +111,12 @@ def lib(build_if_missing: bool = True):
     L.kmd_backward_workspace_bytes.restype = ctypes.c_size_t
     L.kmd_decode_filter_fuse_backward.argtypes = [P, P, P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
     L.kmd_decode_filter_fuse_band.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, P]
+    L.kmd_decode_filter_fuse_band_part.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, i32, i32, C, i32, P]
+    L.kmd_nccl_unique_id.argtypes = [P]
+    L.kmd_comm_init.argtypes = [PP, P, i32, i32]
+    L.kmd_comm_destroy.argtypes = [P]
+    L.kmd_halo_exchange.argtypes = [P, PP, i32, i32, i32, i32, i32, i32, P]
+    L.kmd_band_step.argtypes = [P, P, P, P, P, i32, i32, i32, i32, i32, i32, i32, i32, C, P, P]
     L.kmd_host_workspace_bytes.argtypes = [i32, i32, i32, C]
     L.kmd_host_workspace_bytes.restype = ctypes.c_size_t
     L.kmd_decode_filter_fuse_host.argtypes = [P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
@@ -127,7 +135,9 @@ def lib(build_if_missing: bool = True):
               "kmd_remodulate", "kmd_decode_filter", "kmd_fuse", "kmd_mr_decode_filter_fuse",
               "kmd_downsample2x2", "kmd_combine_resolutions", "kmd_decode_filter_fuse_backward",
               "kmd_temporal_accumulate",
-              "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host"):
+              "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_host",
+              "kmd_decode_filter_fuse_band_part", "kmd_nccl_unique_id", "kmd_comm_init", "kmd_comm_destroy",
+              "kmd_halo_exchange", "kmd_band_step"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -272,6 +282,91 @@ def decode_filter_fuse_band(radiance: torch.Tensor, importance: torch.Tensor,
     _check(lib().kmd_decode_filter_fuse_band(rp, ip, bp, op, N, band_rows, W, halo_top, halo_bot,
                                              y0, H_global, ctypes.byref(cfg),
                                              _stream(radiance, stream)))
+    return out
+
+
+BAND_ALL, BAND_INTERIOR, BAND_SEAMS = 0, 1, 2
+
+
+def decode_filter_fuse_band_part(radiance: torch.Tensor, importance: torch.Tensor,
+                                 blend: Optional[torch.Tensor], sizes: Sequence[int], part: int, *,
+                                 y0: int, band_rows: int, halo_top: int, halo_bot: int, H_global: int,
+                                 out: torch.Tensor, blend_is_logits: bool = True,
+                                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """One part of a row band (BAND_INTERIOR: rows that read owned rows only;
+    BAND_SEAMS: the rest; BAND_ALL: both) into ``out`` [N,3,band_rows,W]."""
+    N, _, R, W = radiance.shape
+    M = len(sizes)
+    assert R == halo_top + band_rows + halo_bot, "radiance rows != halo_top+band_rows+halo_bot"
+    rp = _dev_f32("radiance", radiance, (N, 3, R, W))
+    ip = _dev_f32("importance", importance, (N, M, R, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, band_rows, W))
+    op = _dev_f32("out", out, (N, 3, band_rows, W))
+    cfg = make_config(sizes, blend_is_logits)
+    _check(lib().kmd_decode_filter_fuse_band_part(rp, ip, bp, op, N, band_rows, W, halo_top, halo_bot,
+                                                  y0, H_global, ctypes.byref(cfg), int(part),
+                                                  _stream(radiance, stream)))
+    return out
+
+
+# ------------------------------------------- NCCL row-band exchange (configs[3])
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to every rank)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().kmd_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """An NCCL communicator owned by libkmd's caller (kmd_comm_init / kmd_comm_destroy)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        assert len(uid) == 128
+        self.handle = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().kmd_comm_init(ctypes.byref(self.handle), buf, nranks, rank))
+        self.nranks, self.rank = nranks, rank
+
+    def destroy(self):
+        if self.handle:
+            _check(lib().kmd_comm_destroy(self.handle))
+            self.handle = ctypes.c_void_p()
+
+
+def halo_exchange(comm: Comm, planes: Sequence[torch.Tensor], band_rows: int, halo: int,
+                  peer_up: int, peer_down: int, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """kmd_halo_exchange over contiguous [halo_top + band_rows + halo_bot, W] CUDA planes."""
+    if not planes:
+        return
+    W = planes[0].shape[-1]
+    ptrs = (ctypes.c_void_p * len(planes))(*[_dev_f32(f"planes[{k}]", t) for k, t in enumerate(planes)])
+    _check(lib().kmd_halo_exchange(comm.handle if comm else None, ptrs, len(planes), band_rows, W, halo,
+                                   peer_up, peer_down, _stream(planes[0], stream)))
+
+
+def band_step(comm: Optional[Comm], radiance: torch.Tensor, importance: torch.Tensor,
+              blend: Optional[torch.Tensor], sizes: Sequence[int], out: torch.Tensor, *,
+              y0: int, band_rows: int, halo: int, peer_up: int, peer_down: int, H_global: int,
+              blend_is_logits: bool = True, stream: Optional[torch.cuda.Stream] = None,
+              comm_stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """kmd_band_step: halo exchange on ``comm_stream`` overlapped with the band
+    interior on ``stream``, then the seams.  radiance / importance hold
+    [N, C, halo_top + band_rows + halo_bot, W] with halo_top = halo if
+    peer_up >= 0 else 0 (likewise the bottom)."""
+    N, _, R, W = radiance.shape
+    M = len(sizes)
+    top = halo if peer_up >= 0 else 0
+    bot = halo if peer_down >= 0 else 0
+    assert R == top + band_rows + bot, "radiance rows != halo_top + band_rows + halo_bot"
+    rp = _dev_f32("radiance", radiance, (N, 3, R, W))
+    ip = _dev_f32("importance", importance, (N, M, R, W))
+    bp = None if blend is None else _dev_f32("blend", blend, (N, M, band_rows, W))
+    op = _dev_f32("out", out, (N, 3, band_rows, W))
+    cfg = make_config(sizes, blend_is_logits)
+    cs = None if comm_stream is None else comm_stream.cuda_stream
+    _check(lib().kmd_band_step(comm.handle if comm else None, rp, ip, bp, op, N, band_rows, W, halo,
+                               peer_up, peer_down, y0, H_global, ctypes.byref(cfg),
+                               _stream(radiance, stream), cs))
     return out
 
 

@@ -10,6 +10,6 @@ for f in $ROOT/paper_2202_05977_b200/csrc/*.cu; do
        --expt-relaxed-constexpr $EXTRA -I $ROOT/include -c $f -o $TMP/$(basename $f .cu).o &
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $OUT/libkmd_$NAME.so $TMP/*.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $OUT/libkmd_$NAME.so $TMP/*.o -ldl
 rm -rf $TMP
 echo built $OUT/libkmd_$NAME.so
