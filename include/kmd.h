@@ -40,7 +40,7 @@
  *      100+M, 150+M, 200+M): per output PIXEL.  A pixel is recomputed by a
  *      per-window max-shifted evaluation (IEEE expf and division) when, for
  *      any size, its box denominator sum_q exp(I(q)) lies outside
- *      [1e-30, 1e36] (this includes overflow to +inf), when the sum of its
+ *      [1e-30, 1e30] (this includes overflow to +inf), when the sum of its
  *      fusion weights exp(B_i) lies outside [1e-30, 1e30], or when its result
  *      is not finite.
  *      Other kernels (kmd_last_kernel() 1, 2): per (tile, size).  A tile whose

@@ -45,36 +45,44 @@ def is_stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not (force or is_stale()):
-        return LIB
+CHECKED_LIB = os.path.join(PKG, "libkmd_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Build libkmd.so, or (checked=True) libkmd_checked.so: the same sources
+    with -DKMD_CHECKS (device-side bounds assertions, kmd_common.cuh)."""
+    lib = CHECKED_LIB if checked else LIB
+    if not (force or (is_stale() if not checked else not os.path.exists(lib) or
+                      any(os.path.getmtime(p) > os.path.getmtime(lib) for p in _deps()))):
+        return lib
     nvcc = nvcc_path()
     objs = []
     log_lines = []
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(PKG, "build_checked" if checked else "build")
     os.makedirs(build_dir, exist_ok=True)
+    extra = ["-DKMD_CHECKS"] if checked else []
     for src in sources():
         obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log_lines.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log_lines.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link of libkmd.so failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     with open(os.path.join(build_dir, "build.log"), "w") as f:
         f.write("\n".join(log_lines))
     if verbose:
         print("\n".join(log_lines))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -673,6 +673,41 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
             return cuda_fail(e, "downsample launch");
     if (L == 1) return kmd_decode_filter_fuse(r[0], importance[0], blend ? blend[0] : nullptr, out, N, H, W,
                                               &cfg->level[0], stream);
+    // Fused path (the paper's configuration: every level M = 2 sizes <= 13 with
+    // fusion logits, TMA-compatible widths and alignment): from the coarsest
+    // level up, each level's kernel applies Eq. 7 with the level below in its
+    // epilogue (28-row tiles, kmd_tma_mr.cu), so no fine-level filtered image
+    // makes a round trip through HBM and no separate combine runs.
+    {
+        bool fused = true;
+        uintptr_t amask = (uintptr_t)out;
+        for (int l = 0; l < L && fused; ++l) {
+            const kmd_config& lc = cfg->level[l];
+            fused = lc.num_sizes == 2 && lc.blend_is_logits && blend && blend[l] && ((W >> l) % 4) == 0 &&
+                    (l == L - 1 || (((H >> l) % 2) == 0 && ((W >> l) % 2) == 0));
+            for (int i = 0; i < lc.num_sizes && fused; ++i) fused = lc.sizes[i] <= 13;
+            if (fused) amask |= (uintptr_t)r[l] | (uintptr_t)importance[l] | (uintptr_t)blend[l] | (uintptr_t)f[l] |
+                                (l < L - 1 ? (uintptr_t)alpha[l] : 0);
+        }
+        if (fused && (amask & 15) == 0) {
+            for (int l = L - 1; l >= 0; --l) {
+                kmd::FusedParams p{};
+                p.rad = r[l]; p.imp = importance[l]; p.blend = blend[l];
+                p.out = l == 0 ? out : f[l];
+                p.N = N; p.W = W >> l; p.H = H >> l;
+                p.row_base = 0; p.buf_rows = p.H; p.out_y0 = 0; p.out_rows = p.H;
+                const kmd_config& lc = cfg->level[l];
+                p.M = lc.num_sizes; p.rmax = rmax_of(&lc); p.blend_is_logits = lc.blend_is_logits;
+                for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < lc.num_sizes ? lc.sizes[i] : 1;
+                if (l < L - 1) {
+                    p.cmb_coarse = f[l + 1];  // the combined next-coarser level (the coarsest: as filtered)
+                    p.cmb_alpha = alpha[l];
+                }
+                if ((e = kmd::launch_fused_tma_mr(p, st)) != cudaSuccess) return cuda_fail(e, "MR level launch");
+            }
+            return KMD_OK;
+        }
+    }
     // The coarse levels (and their Eq. 7 combines) run on an auxiliary stream,
     // concurrently with level 0, each persistent launch on its share of the SMs
     // (proportional to its tiles): the small levels no longer run alone.

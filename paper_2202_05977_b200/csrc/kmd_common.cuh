@@ -4,6 +4,27 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+
+// Checked builds (-DKMD_CHECKS, scripts/build_variant.sh checked -DKMD_CHECKS):
+// device-side bounds / protocol assertions on every shared-memory index the
+// pipelined kernels compute, trapping on a violation (compute-sanitizer is not
+// available on this run's GPU pool; tests/test_gpu_checked.py runs the parity
+// suite against the checked build).  Compiled out otherwise.
+#ifdef KMD_CHECKS
+#define KMD_CHECK(cond)                                                                              \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("KMD_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+                   (int)blockIdx.x, (int)threadIdx.x);                                               \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define KMD_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 #include "../../include/kmd.h"
 
@@ -44,6 +65,11 @@ struct FusedParams {
     const float* lse;    // [N,H,W] log sum_i exp(B_i) per pixel, or nullptr (pass A's softmax)
     // imp / blend hold bf16 bits (kmd_decode_filter_fuse_bf16; TMA kernel only)
     int in16;
+    // "Ours MR" (Eq. 7) combine epilogue: out = f + alpha (U coarse - U D f),
+    // with f this launch's fused result, coarse the combined next-coarser level
+    // [N,3,H/2,W/2] and alpha [N,1,H,W] (whole frames, H and W even)
+    const float* cmb_coarse;
+    const float* cmb_alpha;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
@@ -112,6 +138,11 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
     const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
     return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {  // FMNMX3 (sm_100)
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
 }
 __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, <= 1 ulp
     float y;

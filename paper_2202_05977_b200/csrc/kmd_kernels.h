@@ -15,6 +15,9 @@ cudaError_t launch_fused_ws(FusedParams p, cudaStream_t stream);
 bool tma_supported(const FusedParams& p);
 cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream);
 int tma_tile_rows();  // output rows per TMA-kernel tile (the global tile grid's pitch)
+// the same kernel with 28-row tiles and the Eq. 7 combine epilogue (kmd_tma_mr.cu)
+int tma_mr_tile_rows();
+cudaError_t launch_fused_tma_mr(FusedParams p, cudaStream_t stream);
 
 // fusion only, Eq. 5 (kmd_fuse.cu)
 cudaError_t launch_fuse_only(const float* filtered, const float* blend, float* out, int N,
@@ -56,7 +59,7 @@ void api_clear_error();
 
 // kernel variant of the last fused launch on this host thread (kmd_last_kernel)
 enum LastKernel { LK_NONE = 0, LK_DIRECT = 1, LK_WS = 2, LK_TMA = 3, LK_BWD_TILE = 10, LK_BWD_TMA = 11, LK_TMA_SPEC = 100,
-                  LK_TMA_SPEC_ALB = 150, LK_TMA_BF16 = 200 };
+                  LK_TMA_SPEC_ALB = 150, LK_TMA_BF16 = 200, LK_TMA_MR = 300, LK_TMA_MR_CMB = 301 };
 void set_last_kernel(int k);
 
 }  // namespace kmd

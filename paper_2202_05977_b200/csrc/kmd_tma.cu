@@ -38,8 +38,15 @@
 #include "kmd_gw.cuh"
 #include "kmd_kernels.h"
 
+// The file is compiled twice: as itself (namespace tma, 27-row tiles: 1080p
+// is 37 x 40 tiles = 10 per SM) and from kmd_tma_mr.cu (KMD_TMA_SECONDARY,
+// namespace tma28, 28-row tiles whose 2 x 2 blocks never straddle tiles: the
+// multi-resolution levels with the Eq. 7 combine in the epilogue).
+#ifndef KMD_TMA_NS
+#define KMD_TMA_NS tma
+#endif
 namespace kmd {
-namespace tma {
+namespace KMD_TMA_NS {
 
 // development switches (role isolation / ablation probes, env KMD_DEBUG): only
 // in builds with -DKMD_DEBUG_SWITCHES, compiled out of the production kernel
@@ -70,9 +77,12 @@ constexpr int FH = TH + 2 * RMAX;   // 39 field rows in every box
 // -8 works), and 68 columns cover x0-6 .. x0+57 (and the 52 output columns).
 constexpr int XOFF = 8;             // box column 0 = global x0 - XOFF
 constexpr int BW = 68;              // box width
-// V row stride (float4s): SEG 7 reads a row's 8 segments per quarter warp, so
-// any stride is conflict-free (64: no padding); SEG 9 / 13 need 70 / 68
-constexpr int VS = KMD_SEG == 9 ? 70 : KMD_SEG == 13 ? 68 : 64;
+// V row stride (float4s): SEG 9 needs 70 (6 mod 8) and SEG 13 68 (4 mod 8);
+// SEG 7 reads one row per quarter warp, so any stride is conflict-free (64)
+#ifndef KMD_VS
+#define KMD_VS (KMD_SEG == 9 ? 70 : KMD_SEG == 13 ? 68 : 64)
+#endif
+constexpr int VS = KMD_VS;
 // Fusion segments: a fusion thread owns SEG consecutive output pixels of one
 // tile row (NSEG segments per row).  Segment starts are distinct mod 8 (and,
 // with the V row stride VS below, any 8 consecutive fusion threads start in 8
@@ -92,22 +102,57 @@ __host__ __device__ constexpr int seg_len(int sub) {
 // Radiance in tensor memory (KMD_TMEM_RAD 1): each field warp copies its
 // 32 radiance columns of the tile from the (single) shared-memory box into its
 // TMEM quadrant once per tile and its size jobs read them back with tcgen05.ld;
-// the freed box buys the fourth V slot.  0: every job reads the radiance from
-// a double-buffered shared-memory box.
+// the freed box buys the fourth V slot.  0 (default): every job reads the
+// radiance from a double-buffered shared-memory box.  Measured on the B200
+// (1080p, M = 6): 66.1 us with TMEM (V ring 3 or 4 deep, importance ring 3 or
+// 4: no difference) against 57.0 us without -- the tcgen05.ld round trip
+// lengthens the field warps' dependency chains, which are the critical path.
 #ifndef KMD_TMEM_RAD
-#define KMD_TMEM_RAD 1
+#define KMD_TMEM_RAD 0
 #endif
 constexpr bool TMEM_RAD = KMD_TMEM_RAD;
 constexpr int NRAD = TMEM_RAD ? 1 : 2;  // radiance boxes in shared memory
 #ifndef KMD_NI
 #define KMD_NI 3
 #endif
+// V ring depth 4: the field warps (2 sizes in flight) wait less for the
+// fusion warps to free a slot (measured 56.8 vs 58.9 us with 3 slots per
+// 1080p frame; the importance ring depth, 3 to 6, made no difference).  It
+// fits because the tile's output is staged in the V slot of its last size (no
+// separate stage buffer) and the blend boxes are 52 wide.
 #ifndef KMD_NV
-#define KMD_NV (KMD_TMEM_RAD ? 4 : 3)
+#define KMD_NV 4
 #endif
+#ifndef KMD_NB
+#define KMD_NB 4
+#endif
+// exp(I) of each importance box computed by the fusion warps, in place, two
+// steps ahead (EPRE 1), so that the field warps read e directly.  Off: measured
+// 70.3 us (1 step ahead 74.1, 3 steps 110) against 56.9 us with the exp in the
+// field warps -- the fusion warps are not idle enough to absorb it, and the
+// extra hand-off delays the V ring.  (fp32 forward kernels only.)
+#ifndef KMD_EPRE
+#define KMD_EPRE 0
+#endif
+#ifndef KMD_EPRE_AHEAD
+#define KMD_EPRE_AHEAD 2
+#endif
+constexpr int EPRE_AHEAD = KMD_EPRE_AHEAD;
+// blend logits issued by a second producer lane (1) or by the importance
+// producer, in step order (0, default: measured 57.0 vs 58.6 us per 1080p frame)
+#ifndef KMD_BLANE
+#define KMD_BLANE 0
+#endif
+constexpr bool BLANE = KMD_BLANE;
 constexpr int NI = KMD_NI;          // input (importance) ring depth
-constexpr int NB = 4;               // blend ring depth (TMA -> fusion)
+constexpr int NB = KMD_NB;          // blend ring depth (TMA -> fusion)
 constexpr int NV = KMD_NV;          // V ring depth (field -> fusion)
+// L2 prefetch distance in tiles (0 = off): the producer prefetches the boxes
+// of tile tl + L2PF into L2 when it starts tile tl
+#ifndef KMD_L2PF
+#define KMD_L2PF 0
+#endif
+constexpr int L2PF = KMD_L2PF;
 constexpr unsigned TMEM_COLS = 256; // 4 columns (r, g, b, -) per box row: 4 x 39 <= 256
 // field warps; a field job is one (tile, size, 32-column half) walk, and the
 // jobs of consecutive tiles are dealt to the field warps round-robin in one
@@ -178,7 +223,16 @@ template <bool IN16>
 struct InElem {
     using T = float;
     static constexpr int IW = BW;
-    static constexpr int BBW = ROWMAP ? 60 : SEG == 13 ? 52 : 56;  // blend box width (multiple of 4: 16-byte TMA rows)
+    // blend box width (a multiple of 4: 16-byte TMA rows; >= every segment's
+    // reach).  27-row tiles: 52, so the 4-deep blend ring fits beside the
+    // 4-deep V ring (the row map then costs 56 instead of 49 LDS wavefronts
+    // per warp and size; 60 was conflict-free: measured 56.0 vs 56.8 us for
+    // 52 x 4 slots vs 60 x 3 slots per 1080p frame)
+#ifdef KMD_BBW
+    static constexpr int BBW = KMD_BBW;
+#else
+    static constexpr int BBW = SEG == 7 && TH == 27 ? 52 : SEG == 13 ? 52 : 56;
+#endif
 };
 template <>
 struct InElem<true> {
@@ -220,12 +274,17 @@ struct SmemT {
     InSlotT<IN16> in[NI];
     Slot slot[NV];
     BSlotT<IN16> bl[NB];
-    float stage[3][TH][TW];
-    unsigned long long rad_full[NRAD], rad_empty[NRAD], in_full[NI], in_empty[NI], v_full[NV], v_empty[NV],
+    unsigned long long rad_full[NRAD], rad_empty[NRAD], in_full[NI], in_empty[NI], e_full[NI], v_full[NV], v_empty[NV],
         b_full[NB], b_empty[NB];
     unsigned tmem_base;                // TMEM address of the allocation (TMEM_RAD)
 };
 using Smem = SmemT<false>;
+// The staged output tile [3][TH][TW] (backward pass A: [2][TH][TW]) lives in
+// the V slot of the size just consumed (dense layout for the TMA store).
+static_assert(3 * TH * TW * sizeof(float) <= sizeof(Slot), "output tile fits a V slot");
+__device__ __forceinline__ float (*stage_of(Slot& sl))[TH][TW] {
+    return reinterpret_cast<float (*)[TH][TW]>(&sl.V[0][0]);
+}
 static_assert(sizeof(SmemT<false>) <= 232448 && sizeof(SmemT<true>) <= 232448, "227 KB of shared memory per CTA");
 static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InSlotT<false>) % 128 == 0 &&
                   sizeof(BSlotT<false>) % 128 == 0 && sizeof(InSlotT<true>) % 128 == 0 &&
@@ -255,6 +314,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+// L2 prefetch of a box (cp.async.bulk.prefetch.tensor): fire and forget
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                      reinterpret_cast<uint64_t>(tm)),
@@ -263,6 +329,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
@@ -307,11 +374,12 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
 // copied to TMEM); the boxes in shared memory are never written by the
 // generic proxy.  tm: this warp's TMEM quadrant (TMEM_RAD), box row f's
 // (r, g, b) at columns 4f .. 4f+2.
-template <int R, bool CLAMP, class SM, class IS>
+template <int R, bool CLAMP, bool EXPF, class SM, class IS>
 __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci, int top,
                                           int bot, unsigned tm) {
     constexpr int IW = sizeof(in.I[0]) / sizeof(in.I[0][0]);
     const int c = h * 32 + (threadIdx.x & 31);
+    KMD_CHECK(cc >= 0 && cc < BW && ci >= 0 && ci < IW && c < 64 && rb >= 0 && rb < NRAD);
     const auto* Ib = &in.I[0][ci];
     const float* Rb = &sm.rad[rb].v[0][0][cc];
     float4* Vc = &sl.V[0][c];
@@ -320,6 +388,7 @@ __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb
         // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
         // (one STS.128 would halve the store wavefronts but costs MOVs to
         // assemble the quad: measured 7% slower)
+        KMD_CHECK(oy >= 0 && oy < TH);
         const unsigned a = smem_u32(&Vc[oy * VS]);
         asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
         asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
@@ -336,6 +405,7 @@ __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb
                     tmem_ld3(tm + 4 * row, dst[t]);  // (r, g, b) -> .x .y .z
                     // e = exp(I) once per field pixel (Eq. 3's shared weight), in .w
                     // while the TMEM loads are in flight
+                    KMD_CHECK(row >= 0 && row < FH && (!CLAMP || (top < bot && top >= 0 && bot <= FH)));
                     dst[t].w = exp_acc(ld_in(Ib + (CLAMP ? clampi(row, top, bot - 1) : row) * IW));
                 }
                 tmem_wait_ld();
@@ -352,9 +422,11 @@ __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb
         gw_line_field<R, TH>(
             [&](int f) {
                 const int row = CLAMP ? clampi(RMAX - R + f, top, bot - 1) : RMAX - R + f;
+                KMD_CHECK(row >= 0 && row < FH);
                 const float v = ld_in(Ib + row * IW);
                 const float r = Rb[row * BW], g = Rb[FH * BW + row * BW], b = Rb[2 * FH * BW + row * BW];
-                const float e = exp_acc(v);  // once per field pixel (Eq. 3's shared weight)
+                // e = exp(I) once per field pixel (Eq. 3's shared weight); EPRE: already in the box
+                const float e = EXPF ? exp_acc(v) : v;
                 const float2 gb = __fmul2_rn(make_float2(e, e), make_float2(g, b));  // pairs (e, er), (eg, eb)
                 return make_float4(e, e * r, gb.x, gb.y);
             },
@@ -381,17 +453,35 @@ __device__ __forceinline__ void rad_to_tmem(const RadBuf& rad, int cc, int top, 
     tmem_wait_st();
 }
 
-template <bool CLAMP, class SM, class IS>
+template <bool CLAMP, bool EXPF, class SM, class IS>
 __device__ __forceinline__ void field_dispatch(int R, SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci,
                                                int top, int bot, unsigned tm) {
     switch (R) {
-        case 0: field_job<0, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 1: field_job<1, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 2: field_job<2, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 3: field_job<3, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 4: field_job<4, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 5: field_job<5, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        default: field_job<6, CLAMP>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 0: field_job<0, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 1: field_job<1, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 2: field_job<2, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 3: field_job<3, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 4: field_job<4, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 5: field_job<5, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        default: field_job<6, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+    }
+}
+
+// EPRE: e = exp(I) in place over box rows [6-R, 33+R) (every row a size-R
+// field job reads, clamped or not) and all BW columns, float4-wide, by the
+// NFUSE fusion warps (thread c of them).
+template <class IS>
+__device__ __forceinline__ void exp_box(IS& in, int R, int c) {
+    float4* b = reinterpret_cast<float4*>(&in.I[RMAX - R][0]);
+    const int n = (TH + 2 * R) * (BW / 4);
+#pragma unroll 1
+    for (int k = c; k < n; k += NFUSE * 32) {
+        float4 v = b[k];
+        v.x = exp_acc(v.x);
+        v.y = exp_acc(v.y);
+        v.z = exp_acc(v.z);
+        v.w = exp_acc(v.w);
+        b[k] = v;
     }
 }
 
@@ -404,16 +494,16 @@ struct Acc {
 // at a time: a_i = exp(B_i) (unshifted: any shift cancels in the softmax,
 // reading R2), acc += a_i R_i, S += a_i, and Rhat = acc / S at the end.  A
 // logit beyond the fp32 exp range (S = 0 or inf, non-finite acc) or a box
-// denominator outside [1e-30, 1e36] sends the pixel to the exact path (reading
+// denominator outside [1e-30, 1e30] sends the pixel to the exact path (reading
 // R13).
 enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2, FUSE_BWD_H = 3 };
 
 template <int MODE>
 __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alpha */, float4 v) {
     const float rden = rcp_approx(v.x);
-    // range flag (reading R13): den < 1e-30 or den > 1e36 (then rden < 1e-36;
+    // range flag (reading R13): den < 1e-30 or den > 1e30 (then rden < 1e-30;
     // rcp.approx.ftz of den >= 2^126 or inf is 0) ends below 1e-30 here
-    st.dmin[j] = fminf(st.dmin[j], fminf(v.x, rden * 1e6f));
+    st.dmin[j] = fmin3(st.dmin[j], v.x, rden);
     float w;
     if constexpr (MODE == FUSE_ONE) {
         w = rden;
@@ -424,8 +514,9 @@ __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alph
     } else {  // alpha given (blend_is_logits == 0)
         w = a * rden;
     }
-    st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
-    st.a[j][1] = fmaf(w, v.z, st.a[j][1]);
+    const float2 a01 = __ffma2_rn(make_float2(w, w), make_float2(v.y, v.z), make_float2(st.a[j][0], st.a[j][1]));
+    st.a[j][0] = a01.x;
+    st.a[j][1] = a01.y;
     st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
 }
 
@@ -440,6 +531,7 @@ __device__ __forceinline__ void fuse_seg(Acc& st, const T* Br, const float4 (&o)
 // follows exists once -- keeps the fusion warps' hot code small).
 template <int R>
 __device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)[SEG]) {
+    KMD_CHECK(ty >= 0 && ty < TH && xs + RMAX - R >= 0 && xs + RMAX + R + SEG <= VS);
     const float4* Vr = &sl.V[ty][xs + RMAX - R];
     gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
 }
@@ -457,6 +549,7 @@ __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, c
         case 5: hbox<5>(sl, ty, xs, o); break;
         default: hbox<6>(sl, ty, xs, o); break;
     }
+    KMD_CHECK(xb >= 0 && xb + SEG <= (int)(sizeof(bs.B[0]) / sizeof(bs.B[0][0])));
     const auto* Br = &bs.B[ty][xb];
     if constexpr (SMODE >= 0) {
         fuse_seg<SMODE>(st, Br, o);  // mode fixed by the kernel's specialisation
@@ -531,12 +624,14 @@ struct Runtime {
     static constexpr int MODE = -1;
     static constexpr bool ALB = true;
     static constexpr bool IN16 = false;
+    static constexpr bool CMB = false;
 };
 struct Runtime16 {  // bf16 importance / logits, any M (NEXT row 4's alternative)
     static constexpr int M = 0;
     static constexpr int MODE = -1;
     static constexpr bool ALB = true;
     static constexpr bool IN16 = true;
+    static constexpr bool CMB = false;
 };
 // backward pass A (NEXT row 3): the forward's tiles and box sums, with the
 // fusion epilogue replaced by the per-size gradient field h_i (runtime M)
@@ -545,13 +640,15 @@ struct SpecBwdH {
     static constexpr int MODE = FUSE_BWD_H;
     static constexpr bool ALB = false;
     static constexpr bool IN16 = false;
+    static constexpr bool CMB = false;
 };
-template <int MODE_, bool ALB_, int M_, bool IN16_ = false>
+template <int MODE_, bool ALB_, int M_, bool IN16_ = false, bool CMB_ = false>
 struct Spec {
     static constexpr int MODE = MODE_;  // FUSE_SOFTMAX (blend logits)
     static constexpr bool ALB = ALB_;   // albedo epilogue (NEXT row 1)
     static constexpr int M = M_;
     static constexpr bool IN16 = IN16_;  // bf16 importance / logits
+    static constexpr bool CMB = CMB_;    // Eq. 7 combine epilogue (NEXT row 2, "Ours MR"; even TH)
 };
 
 // --------------------------------------------------------------------- kernel
@@ -568,6 +665,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     SmemK& sm = *reinterpret_cast<SmemK*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = SP::M > 0 ? SP::M : p.M;
+    constexpr bool EPRE = KMD_EPRE && !SP::IN16 && SP::MODE != FUSE_BWD_H && !TMEM_RAD;
     const bool has_blend = p.blend != nullptr && !(KMD_DBG(16));
     unsigned rpack = 0;  // radius of size i in bits 4i..4i+3
     for (int i = 0; i < M; ++i) rpack |= (unsigned)((p.sizes[i] - 1) / 2) << (4 * i);
@@ -579,6 +677,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int s = 0; s < NI; ++s) {
             mbar_init(&sm.in_full[s], 1);
+            mbar_init(&sm.e_full[s], NFUSE);             // every fusion warp's share of exp(I) (EPRE)
             mbar_init(&sm.in_empty[s], 2);              // both halves (one elected lane each)
         }
         for (int s = 0; s < NV; ++s) {
@@ -616,16 +715,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_imp)) : "memory");
             }
             constexpr unsigned ESZ = SP::IN16 ? 2 : 4;
-            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * InElem<SP::IN16>::IW * ESZ,
-                               B_BYTES = TH * InElem<SP::IN16>::BBW * ESZ;
+            constexpr unsigned RAD_BYTES = 3 * FH * BW * 4, I_BYTES = FH * InElem<SP::IN16>::IW * ESZ;
             // In-order, blocking issue of every (tile, size) step: radiance
-            // (per tile), importance and blend logits.  Deadlock-free: each wait
-            // is on a slot released by a step whose inputs were issued earlier
-            // (the field warps run at most NV steps ahead of the fusion warps,
-            // and the rings are NI, NB >= NV + 1 deep).
+            // (per tile) and importance (lane 1: the blend logits).
+            // Deadlock-free: each wait is on a slot released by a step whose
+            // inputs were issued earlier.
             for (int tl = 0; tl < my_tiles; ++tl) {
                 const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
                 const int rb = tl % NRAD;
+                if (L2PF > 0 && tl + L2PF < my_tiles) {
+                    // HBM -> L2 prefetch of a later tile's boxes (no shared memory,
+                    // no barrier): its TMA loads then hit L2
+                    const Tile pf = tile_of(p, blockIdx.x + (tl + L2PF) * gridDim.x, tiles_x, tiles_y);
+                    tma_prefetch_3d(&tm_rad, pf.x0 - XOFF, pf.y0 - RMAX - p.row_base, pf.n * 3);
+                    for (int i = 0; i < M; ++i) {
+                        tma_prefetch_3d(&tm_imp, pf.x0 - XOFF - xalign<SP::IN16>(pf.x0), pf.y0 - RMAX - p.row_base,
+                                        pf.n * M + i);
+                        if (has_blend)
+                            tma_prefetch_3d(&tm_blend, pf.x0 - xalign<SP::IN16>(pf.x0), pf.y0 - p.out_y0, pf.n * M + i);
+                    }
+                }
                 IWAIT(0, mbar_wait(&sm.rad_empty[rb], ((tl / NRAD) & 1) ^ 1));
                 if (KMD_DBG(256)) {
                     mbar_arrive(&sm.rad_full[rb]);
@@ -644,13 +753,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         tma_load_3d(&sm.in[s].I[0][0], &tm_imp, tc.x0 - XOFF - xalign<SP::IN16>(tc.x0),
                                     tc.y0 - RMAX - p.row_base, tc.n * M + i, &sm.in_full[s]);
                     }
-                    if (has_blend) {
+                    if (!BLANE && has_blend) {
+                        constexpr unsigned B_BYTES = TH * InElem<SP::IN16>::BBW * ESZ;
                         const int sb = seq % NB;
                         IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
                         mbar_arrive_expect_tx(&sm.b_full[sb], B_BYTES);
                         tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0 - xalign<SP::IN16>(tc.x0),
                                     tc.y0 - p.out_y0, tc.n * M + i, &sm.b_full[sb]);
                     }
+                }
+            }
+        } else if (BLANE && lane == 1 && has_blend) {
+            // the blend logits from a second producer thread, so the importance
+            // stream (field warps, ahead) never waits behind a blend slot that
+            // the fusion warps (behind) have not released yet
+            constexpr unsigned ESZ = SP::IN16 ? 2 : 4;
+            constexpr unsigned B_BYTES = TH * InElem<SP::IN16>::BBW * ESZ;
+            for (int tl = 0; tl < my_tiles; ++tl) {
+                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                for (int i = 0; i < M; ++i) {
+                    const int seq = tl * M + i, sb = seq % NB;
+                    IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
+                    mbar_arrive_expect_tx(&sm.b_full[sb], B_BYTES);
+                    tma_load_3d(&sm.bl[sb].B[0][0], &tm_blend, tc.x0 - xalign<SP::IN16>(tc.x0),
+                                tc.y0 - p.out_y0, tc.n * M + i, &sm.b_full[sb]);
                 }
             }
         }
@@ -674,27 +800,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             const int rb = tl % NRAD;
-            const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
-            const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
-            const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
-            const int ci = cc + xalign<SP::IN16>(tc.x0);
             IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl / NRAD) & 1));
             if constexpr (TMEM_RAD) {
-                rad_to_tmem(sm.rad[0], cc, top, bot, tm);
+                const int top = max(0, ylo - (tc.y0 - RMAX)), bot = min(FH, yhi - (tc.y0 - RMAX) + 1);
+                rad_to_tmem(sm.rad[0], clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF), top, bot, tm);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.rad_empty[0]);
             }
 #pragma unroll 1
             for (; g < 2 * M * (tl + 1); g += NFIELD) {
                 const int seq = g >> 1, i = seq - tl * M;
+                // per job (short live ranges: the fusion role sets the register budget)
+                const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
+                const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
+                const int cc = clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF);  // R1 column clamp
+                const int ci = cc + xalign<SP::IN16>(tc.x0);
                 const int si = seq % NI, sv = seq % NV;
                 Slot& sl = sm.slot[sv];
                 auto& in = sm.in[si];
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
-                IWAIT(4, mbar_wait(&sm.in_full[si], (seq / NI) & 1));
+                IWAIT(4, mbar_wait(EPRE ? &sm.e_full[si] : &sm.in_full[si], (seq / NI) & 1));
                 const int R = (rpack >> (4 * i)) & 15;
-                if (top > 0 || bot < FH) field_dispatch<true>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
-                else field_dispatch<false>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                if (top > 0 || bot < FH) field_dispatch<true, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                else field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
                 // one arrive per warp: __syncwarp orders every lane's shared
                 // memory accesses before the elected lane's release-arrive
                 __syncwarp();
@@ -720,6 +848,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int xs = seg_start(sub);
         const int len = seg_len(sub);
         int vs = 0, vph = 0, bs = 0, bph = 0;  // V / blend ring slot and phase of the current step
+        // The output tile is staged in the V slot of the step just consumed and
+        // leaves with a TMA store; that slot goes back to the field warps once
+        // the store has read it.  Fusion warp 0 withholds its arrival on the
+        // slot's v_empty (the other warps arrive as usual) and thread 0 makes it
+        // one step later, after cp.async.bulk.wait_group.read (keep = store
+        // groups allowed to stay in flight: the one issued since).
+        // EPRE: exp(I) of step q's importance box, in place, then e_full
+        auto epre = [&](int q) {
+            if (EPRE && q < my_tiles * M) {
+                const int s_ = q % NI;
+                IWAIT(11, mbar_wait(&sm.in_full[s_], (q / NI) & 1));
+                exp_box(sm.in[s_], (rpack >> (4 * (q % M))) & 15, c);
+                fence_proxy_async();  // generic writes before the slot's next TMA overwrite
+                __syncwarp();
+                if ((c & 31) == 0) mbar_arrive(&sm.e_full[s_]);
+            }
+        };
+        for (int q = 0; q < EPRE_AHEAD; ++q) epre(q);
+        int pend = -1;
+        auto release_pending = [&](int keep) {
+            if (pend >= 0) {
+                if (c == 0) {
+                    if (keep) bulk_wait_read1();
+                    else bulk_wait_read0();
+                    mbar_arrive(&sm.v_empty[pend]);
+                }
+                pend = -1;
+            }
+        };
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
             if constexpr (SP::MODE == FUSE_BWD_H) {
@@ -798,26 +955,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                     __syncwarp();
-                    if ((c & 31) == 0) {  // V and the logits are consumed: release them now
-                        mbar_arrive(&sm.v_empty[vs]);
+                    if ((c & 31) == 0) {  // V and the logits are consumed (warp 0: see pend)
+                        if (c != 0) mbar_arrive(&sm.v_empty[vs]);
                         if (has_blend) mbar_arrive(&sm.b_empty[bs]);
                     }
-                    // the stage is free once the previous size's store has read it
-                    if (c == 0) bulk_wait_read0();
-                    fuse_bar();
+                    fuse_bar();  // every fusion thread is done with V: the slot becomes the stage
+                    auto stage = stage_of(sm.slot[vs]);
                     if (active) {
 #pragma unroll
                         for (int j = 0; j < SEG; ++j)
                             if (j < len) {
-                                sm.stage[0][ty][xs + j] = sv[j];
-                                sm.stage[1][ty][xs + j] = dv[j];
+                                stage[0][ty][xs + j] = sv[j];
+                                stage[1][ty][xs + j] = dv[j];
                             }
                     }
                     fence_proxy_async();
                     fuse_bar();
                     // one TMA store of the pair of planes [2][27][52] (clipped at the frame edge)
                     if (c == 0 && !(KMD_DBG(1)))
-                        tma_store_3d(&tm_out, tc.x0, tc.y0, 2 * (tc.n * M + i), &sm.stage[0][0][0]);
+                        tma_store_3d(&tm_out, tc.x0, tc.y0, 2 * (tc.n * M + i), &stage[0][0][0]);
+                    release_pending(1);  // the previous size's slot (its store has been read)
+                    pend = vs;
                     if (++vs == NV) { vs = 0; vph ^= 1; }
                     if (++bs == NB) { bs = 0; bph ^= 1; }
                 }
@@ -844,7 +1002,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                                     (size_t)gyc * p.W + gxc));
                 }
             }
+            // Eq. 7 combine (CMB, "Ours MR"): the tile's 2 x 2
+            // blocks (even TH and tile origins), thread c owning blocks c,
+            // c + 32 NFUSE: their alphas and the coarse level's value loaded now
+            constexpr int CMBQ = (TH / 2) * (TW / 2), CMBN = (CMBQ + NFUSE * 32 - 1) / (NFUSE * 32);
+            static_assert(!SP::CMB || TH % 2 == 0, "the combine epilogue needs whole 2x2 blocks per tile");
+            float4 cmba[SP::CMB ? CMBN : 1];
+            float cmbc[SP::CMB ? CMBN : 1][3];
+            if constexpr (SP::CMB) {
+                const size_t plane = (size_t)p.H * p.W, cplane = (size_t)(p.H / 2) * (p.W / 2);
+#pragma unroll
+                for (int k = 0; k < CMBN; ++k) {
+                    const int b = min(c + k * NFUSE * 32, CMBQ - 1);
+                    const int by = b / (TW / 2), bx = b - by * (TW / 2);
+                    const int gy = min(tc.y0 + 2 * by, p.H - 2), gx = min(tc.x0 + 2 * bx, p.W - 2);
+                    const float* al = p.cmb_alpha + (size_t)tc.n * plane + (size_t)gy * p.W + gx;
+                    const float2 a0 = __ldg(reinterpret_cast<const float2*>(al));
+                    const float2 a1 = __ldg(reinterpret_cast<const float2*>(al + p.W));
+                    cmba[k] = make_float4(a0.x, a0.y, a1.x, a1.y);
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch)
+                        cmbc[k][ch] = __ldg(p.cmb_coarse + ((size_t)tc.n * 3 + ch) * cplane +
+                                            (size_t)(gy / 2) * (p.W / 2) + gx / 2);
+                }
+            }
             Acc st;
+            int stage_slot = 0;
 #pragma unroll
             for (int j = 0; j < SEG; ++j) {
                 st.S[j] = 0.f;
@@ -853,23 +1036,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
 #pragma unroll 1
             for (int i = 0; i < M; ++i) {
+                epre(tl * M + i + EPRE_AHEAD);
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
                 if (!(KMD_DBG(64)) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
                                                                    (rpack >> (4 * i)) & 15);
                 __syncwarp();
                 if ((c & 31) == 0) {
-                    mbar_arrive(&sm.v_empty[vs]);
+                    // the last size's slot becomes the stage: warp 0 withholds its arrival (pend)
+                    if (!(c == 0 && i == M - 1)) mbar_arrive(&sm.v_empty[vs]);
                     if (has_blend) mbar_arrive(&sm.b_empty[bs]);
                 }
+                if (i == 0) release_pending(0);  // the previous tile's stage slot
+                if (i == M - 1) stage_slot = vs;
                 // ring slots and phases of the next (tile, size) step
                 if (++vs == NV) { vs = 0; vph ^= 1; }
                 if (++bs == NB) { bs = 0; bph ^= 1; }
             }
-            if (KMD_DBG(1024)) continue;
+            if (KMD_DBG(1024)) {
+                pend = stage_slot;
+                continue;
+            }
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
-            if (c == 0) bulk_wait_read0();  // previous tile's store has read the stage
-            IWAIT(9, fuse_bar());
+            IWAIT(9, fuse_bar());  // every fusion thread is done with the last V: it becomes the stage
+            auto stage = stage_of(sm.slot[stage_slot]);
             const int gy = tc.y0 + ty;
             const bool row_ok = gy >= p.out_y0 && gy < p.out_y0 + p.out_rows;
             const bool norm = M > 1 && p.blend_is_logits;
@@ -883,9 +1073,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 bad |= b ? (1u << j) : 0u;
                 if (j < len && active) {
                     float r0 = o0, r1 = o1, r2 = o2;
-                    sm.stage[0][ty][xs + j] = r0;
-                    sm.stage[1][ty][xs + j] = r1;
-                    sm.stage[2][ty][xs + j] = r2;
+                    stage[0][ty][xs + j] = r0;
+                    stage[1][ty][xs + j] = r1;
+                    stage[2][ty][xs + j] = r2;
                 }
             }
             // rare: pixels outside the unshifted exp range -> exact evaluation
@@ -894,9 +1084,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int gx = tc.x0 + xs + j;
                     if (((bad >> j) & 1u) && gx < p.W) {
                         float3 e = exact_pixel(p, tc.n, gx, gy);
-                        sm.stage[0][ty][xs + j] = e.x;
-                        sm.stage[1][ty][xs + j] = e.y;
-                        sm.stage[2][ty][xs + j] = e.z;
+                        stage[0][ty][xs + j] = e.x;
+                        stage[1][ty][xs + j] = e.y;
+                        stage[2][ty][xs + j] = e.z;
+                    }
+                }
+            }
+            if constexpr (SP::CMB) {
+                // o = f - alpha U D f + alpha U c (Eq. 7) as fma(alpha, c - D f, f),
+                // the block mean in kmd_combine_resolutions' order
+                fuse_bar();  // the whole tile (f) is staged
+#pragma unroll
+                for (int k = 0; k < CMBN; ++k) {
+                    const int b = c + k * NFUSE * 32;
+                    const int by = b / (TW / 2), bx = b - by * (TW / 2);
+                    const int r = 2 * by, x = 2 * bx;
+                    if (b < CMBQ && tc.y0 + r < p.H && tc.x0 + x < p.W) {
+                        const float4 a = cmba[k];
+#pragma unroll
+                        for (int ch = 0; ch < 3; ++ch) {
+                            const float f00 = stage[ch][r][x], f01 = stage[ch][r][x + 1];
+                            const float f10 = stage[ch][r + 1][x], f11 = stage[ch][r + 1][x + 1];
+                            const float d = cmbc[k][ch] - 0.25f * ((f00 + f01) + (f10 + f11));
+                            stage[ch][r][x] = fmaf(a.x, d, f00);
+                            stage[ch][r][x + 1] = fmaf(a.y, d, f01);
+                            stage[ch][r + 1][x] = fmaf(a.z, d, f10);
+                            stage[ch][r + 1][x + 1] = fmaf(a.w, d, f11);
+                        }
                     }
                 }
             }
@@ -908,7 +1122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (idx < ALBQ) {
                         const int ch = idx / (TH * (TW / 4)), rem = idx - ch * (TH * (TW / 4));
                         const int r = rem / (TW / 4), q = rem - r * (TW / 4);
-                        float4* sp = reinterpret_cast<float4*>(&sm.stage[ch][r][4 * q]);
+                        float4* sp = reinterpret_cast<float4*>(&stage[ch][r][4 * q]);
                         const float4 v = *sp, a = albv[k];
                         *sp = make_float4(v.x * a.x, v.y * a.y, v.z * a.z, v.w * a.w);
                     }
@@ -920,7 +1134,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // TMA store; it clips the parts beyond W / out_rows.  (A TMA store
                 // with a negative coordinate faults on this B200, so the first tile
                 // of a row band that starts inside a tile is stored by hand below.)
-                if (c == 0 && !(KMD_DBG(1))) tma_store_3d(&tm_out, tc.x0, tc.y0 - p.out_y0, tc.n * 3, &sm.stage[0][0][0]);
+                if (c == 0 && !(KMD_DBG(1))) tma_store_3d(&tm_out, tc.x0, tc.y0 - p.out_y0, tc.n * 3, &stage[0][0][0]);
             } else {
                 float* out = p.out + (size_t)tc.n * 3 * ((size_t)p.out_rows * p.W);
                 for (int idx = c; idx < 3 * TH * TW; idx += NFUSE * 32) {
@@ -928,9 +1142,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int oy = rr / TW, ox = rr - oy * TW;
                     const int yy = tc.y0 + oy, xx = tc.x0 + ox;
                     if (xx < p.W && yy >= p.out_y0 && yy < p.out_y0 + p.out_rows)
-                        out[((size_t)ch * p.out_rows + (yy - p.out_y0)) * p.W + xx] = sm.stage[ch][oy][ox];
+                        out[((size_t)ch * p.out_rows + (yy - p.out_y0)) * p.W + xx] = stage[ch][oy][ox];
                 }
+                fuse_bar();  // every thread is done reading the stage slot
             }
+            pend = stage_slot;  // released after the next tile's first size (or never: kernel end)
         }
         if (c == 0) bulk_wait0();
     }
@@ -983,8 +1199,9 @@ bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long plan
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-}  // namespace tma
+}  // namespace KMD_TMA_NS
 
+#ifndef KMD_TMA_SECONDARY
 #ifdef KMD_INSTR
 extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, tma::g_instr, sizeof(unsigned long long) * n);
@@ -1104,5 +1321,57 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     set_last_kernel(LK_TMA);
     return launch(fused_tma_kernel<Runtime>);
 }
+#else   // KMD_TMA_SECONDARY: the multi-resolution levels (28-row tiles)
+
+int tma_mr_tile_rows() { return KMD_TMA_NS::TH; }
+
+// One "Ours MR" level on the 28-row-tile kernel: the fused decode + filter +
+// fusion of the level's M = 2 sizes (or any M <= 8 at run time) and, when
+// p.cmb_coarse is set, the Eq. 7 combine with the next-coarser combined level
+// in the epilogue (whole frames, H and W even, W % 4 == 0, 16-B aligned).
+cudaError_t launch_fused_tma_mr(FusedParams p, cudaStream_t stream) {
+    using namespace KMD_TMA_NS;
+    p.tile_y_begin = 0;
+    p.tile_rows_a = 0x7fffffff;
+    const int tiles_y = (p.H + TH - 1) / TH, tiles_x = (p.W + TW - 1) / TW;
+    const long long n_tiles = (long long)tiles_x * tiles_y * p.N;
+    if (n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
+    CUtensorMap m_rad, m_imp, m_blend, m_out;
+    if (!make_map(&m_rad, p.rad, p.W, p.H, 3LL * p.N, BW, FH, 3) ||
+        !make_map(&m_imp, p.imp, p.W, p.H, (long long)p.M * p.N, BW, FH, 1) ||
+        !make_map(&m_out, p.out, p.W, p.H, 3LL * p.N, TW, TH, 3))
+        return cudaErrorInvalidValue;
+    if (p.blend) {
+        if (!make_map(&m_blend, p.blend, p.W, p.H, (long long)p.M * p.N, InElem<false>::BBW, TH, 1))
+            return cudaErrorInvalidValue;
+    } else {
+        m_blend = m_imp;
+    }
+    int dev = 0, sms = 148;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    const size_t smem = sizeof(Smem);
+    const int grid = (int)(n_tiles < sms ? n_tiles : sms);
+    auto launch = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
+        return cudaGetLastError();
+    };
+    const bool softmax = p.blend != nullptr && p.blend_is_logits && p.M == 2;
+    if (p.cmb_coarse) {
+        if (!softmax) return cudaErrorInvalidValue;  // the paper's levels: sizes {3, 5} with fusion logits
+        set_last_kernel(LK_TMA_MR_CMB);
+        return launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2, false, true>>);
+    }
+    if (softmax) {
+        set_last_kernel(LK_TMA_MR);
+        return launch(fused_tma_kernel<Spec<FUSE_SOFTMAX, false, 2>>);
+    }
+    set_last_kernel(LK_TMA_MR);
+    return launch(fused_tma_kernel<Runtime>);
+}
+#endif  // KMD_TMA_SECONDARY
 
 }  // namespace kmd

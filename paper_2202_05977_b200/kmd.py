@@ -17,7 +17,9 @@ import torch
 from . import _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkmd.so")
+# KMD_LIB selects another build of the same library (e.g. libkmd_checked.so,
+# the -DKMD_CHECKS build with device-side bounds assertions)
+LIB_PATH = os.environ.get("KMD_LIB") or os.path.join(_HERE, "libkmd.so")
 
 KMD_MAX_SIZES = 8
 KMD_MAX_K = 31
@@ -84,7 +86,7 @@ def lib(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing and _build.is_stale():
+    if build_if_missing and LIB_PATH == _build.LIB and _build.is_stale():
         _build.build()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libkmd.so not found at {LIB_PATH}; run __graft_entry__.build()")
@@ -424,6 +426,8 @@ def last_kernel() -> str:
     v1-direct, v2-ws, v3-tma (runtime M), v3-tma-M<m>[-albedo] (compiled for M),
     v3-tma-bf16[-M<m>] (bf16 importance / logits)."""
     code = int(lib().kmd_last_kernel())
+    if code >= 300:  # the multi-resolution levels' 28-row-tile kernel (+ Eq. 7 combine epilogue)
+        return "v3-tma28-mr-cmb" if code == 301 else "v3-tma28-mr"
     if code >= 200:
         return f"v3-tma-bf16-M{code - 200}" if code > 200 else "v3-tma-bf16"
     if code >= 150:

@@ -1,0 +1,25 @@
+"""The -DKMD_CHECKS build of libkmd (device-side bounds assertions on every
+shared-memory index of the pipelined kernels, kmd_common.cuh KMD_CHECK) runs
+one small case of every kernel family and compares each with the oracle
+(scripts/sanitize_cases.py).  This stands in for compute-sanitizer, which is
+closed on this run's GPU pool; a violated check traps, so the subprocess
+fails."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_checked_build_runs_every_kernel_family():
+    from paper_2202_05977_b200 import _build
+    lib = _build.build(checked=True)
+    env = dict(os.environ, KMD_LIB=lib)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_cases.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "sanitize cases done" in r.stdout, out[-4000:]
+    assert "KMD_CHECK failed" not in out

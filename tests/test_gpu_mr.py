@@ -26,6 +26,10 @@ def test_mr_matches_oracle(oracle_mod, cuda_device, N, H, W):
                                     [_dev(t, cuda_device) for t in mi.blend],
                                     [_dev(t, cuda_device) for t in mi.alpha], sizes)
     torch.cuda.synchronize()
+    # the paper's levels ({3,5} with logits) on TMA-compatible widths take the
+    # fused path: 28-row tiles with Eq. 7 in the epilogue (kmd_tma_mr.cu)
+    if all((W >> l) % 4 == 0 for l in range(3)):
+        assert kmd.last_kernel() == "v3-tma28-mr-cmb"
     ref = oracle_mod.mr_decode_filter_fuse(mi.radiance.numpy(), [t.numpy() for t in mi.importance],
                                            [t.numpy() for t in mi.blend], [t.numpy() for t in mi.alpha],
                                            sizes)
@@ -61,6 +65,10 @@ def test_mr_other_level_counts(oracle_mod, cuda_device, levels, N, H, W):
                                     [t.to(cuda_device) for t in mi.blend],
                                     [t.to(cuda_device) for t in mi.alpha], sizes)
     torch.cuda.synchronize()
+    # the paper's levels ({3,5} with logits) on TMA-compatible widths take the
+    # fused path: 28-row tiles with Eq. 7 in the epilogue (kmd_tma_mr.cu)
+    if levels > 1 and all((W >> l) % 4 == 0 for l in range(levels)):
+        assert kmd.last_kernel() == "v3-tma28-mr-cmb"
     ref = oracle_mod.mr_decode_filter_fuse(mi.radiance.numpy(), [t.numpy() for t in mi.importance],
                                            [t.numpy() for t in mi.blend], [t.numpy() for t in mi.alpha], sizes)
     f0 = oracle_mod.decode_filter_fuse(mi.radiance.numpy(), mi.importance[0].numpy(), mi.blend[0].numpy(),
