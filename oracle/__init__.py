@@ -60,6 +60,8 @@ def _load():
         lib.kmdo_fuse.argtypes = [P, P, i32, i32, i32, i32, P]
         lib.kmdo_decode_filter_fuse_rows.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
                                                      i32, i32, i32, P]
+        lib.kmdo_decode_filter_fuse_rows_f64rad.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
+                                                            i32, i32, i32, P]
         lib.kmdo_decode_filter_fuse_pixels.argtypes = [P, P, P, i32, i32, i32, i32, P, i32,
                                                        P, P, P, ctypes.c_int64, i32, P]
         lib.kmdo_max_threads.argtypes = []
@@ -72,7 +74,8 @@ def _load():
         f32 = ctypes.c_float
         lib.kmdo_temporal_accumulate.argtypes = [P, P, P, P, P, P, P, P, i32, i32, i32, f32, f32, f32, P, P]
         for f in ("kmdo_unfold", "kmdo_kernel_map", "kmdo_apply", "kmdo_fuse",
-                  "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_pixels",
+                  "kmdo_decode_filter_fuse_rows", "kmdo_decode_filter_fuse_rows_f64rad",
+                  "kmdo_decode_filter_fuse_pixels",
                   "kmdo_max_threads", "kmdo_demodulate", "kmdo_remodulate", "kmdo_downsample_2x2",
                   "kmdo_upsample_nearest", "kmdo_combine_resolutions", "kmdo_backward",
                   "kmdo_temporal_accumulate"):
@@ -158,7 +161,8 @@ def decode_filter_fuse(radiance, importance, blend, sizes: Sequence[int],
     """Per-pixel evaluation of Eq. 3 -> 4 -> 5 for radiance [N,3,H,W],
     importance [N,M,H,W], blend [N,M,H,W] (None iff M==1).  Returns fp64
     [N,3,H,W], or [N,3,y1-y0,W] for rows=(y0,y1)."""
-    radiance = _f32(radiance)
+    f64 = isinstance(radiance, np.ndarray) and radiance.dtype == np.float64
+    radiance = np.ascontiguousarray(radiance) if f64 else _f32(radiance)
     importance = _f32(importance)
     b = None if blend is None else _f32(blend)
     N, _, H, W = radiance.shape
@@ -167,9 +171,10 @@ def decode_filter_fuse(radiance, importance, blend, sizes: Sequence[int],
     y0, y1 = (0, H) if rows is None else rows
     sz = np.ascontiguousarray(sizes, dtype=np.int32)
     out = np.empty((N, 3, y1 - y0, W), dtype=np.float64)
-    _check(_load().kmdo_decode_filter_fuse_rows(
-        _ptr(radiance), _ptr(importance), _ptr(b), N, H, W, M, _ptr(sz),
-        int(bool(blend_is_logits)), y0, y1, threads, _ptr(out)))
+    # fp64 radiance (the multi-resolution pyramid levels) is read as given
+    fn = _load().kmdo_decode_filter_fuse_rows_f64rad if f64 else _load().kmdo_decode_filter_fuse_rows
+    _check(fn(_ptr(radiance), _ptr(importance), _ptr(b), N, H, W, M, _ptr(sz),
+              int(bool(blend_is_logits)), y0, y1, threads, _ptr(out)))
     return out
 
 
@@ -225,6 +230,13 @@ def downsample_2x2(img) -> np.ndarray:
     return out
 
 
+def downsample_2x2_f64(img) -> np.ndarray:
+    """D of Eq. 7 on an fp32 or fp64 image, in fp64: the block mean written out
+    (SPEC.md:56-63), for the pyramid's deeper levels."""
+    a = np.asarray(img, dtype=np.float64)
+    return 0.25 * ((a[..., 0::2, 0::2] + a[..., 0::2, 1::2]) + (a[..., 1::2, 0::2] + a[..., 1::2, 1::2]))
+
+
 def upsample_nearest(img) -> np.ndarray:
     """U of Eq. 7: [..., h, w] -> [..., 2h, 2w] (fp64)."""
     a = np.ascontiguousarray(img, dtype=np.float64)
@@ -247,13 +259,12 @@ def combine_resolutions(fine, coarse, alpha) -> np.ndarray:
 
 def mr_decode_filter_fuse(radiance, importance, blend, alpha, sizes, threads: int = 0) -> np.ndarray:
     """"Ours MR": level l filters D^l(radiance) with importance[l], blend[l]
-    (Eq. 3-5), then Eq. 7 combines from the coarsest level.  The downsampled
-    radiance is rounded to fp32 between levels (the GPU path stores it in fp32,
-    so both sides filter the same level inputs)."""
+    (Eq. 3-5), then Eq. 7 combines from the coarsest level.  The pyramid
+    levels D^l(radiance) stay in fp64 (PAPER.md:316-318 defines them exactly)."""
     L = len(importance)
     rad = [_f32(radiance)]
     for _ in range(1, L):
-        rad.append(downsample_2x2(rad[-1]).astype(np.float32))
+        rad.append(downsample_2x2_f64(rad[-1]))
     f = [decode_filter_fuse(rad[l], importance[l], None if blend is None else blend[l], sizes[l],
                             threads=threads) for l in range(L)]
     c = f[L - 1]

@@ -66,13 +66,30 @@ static void softmax_window(const double* u, int kk, double* w) {
 
 /* ---- Step 3: apply (Eq. 4) ----------------------------
  * R(p) = sum_q w_p(q) r(q), "the same weights to each RGB color channel". */
+/* the radiance of one frame as fp32 (the inputs) or fp64 (a downsampled
+ * pyramid level of the multi-resolution variant, kept in fp64) */
+typedef struct {
+    const float* f;
+    const double* d;
+} rad_t;
+static double rad_at(rad_t r, size_t i) { return r.d ? r.d[i] : (double)r.f[i]; }
+static rad_t rad_f32(const float* f) {
+    rad_t r = {f, NULL};
+    return r;
+}
+static rad_t rad_offset(rad_t r, size_t off) {
+    rad_t o = r;
+    if (o.d) o.d += off; else o.f += off;
+    return o;
+}
+
 static void apply_window(const double* w, const int* qy, const int* qx, int kk,
-                         const float* radiance /* [3,H,W] */, int H, int W, double R[3]) {
+                         rad_t radiance /* [3,H,W] */, int H, int W, double R[3]) {
     const size_t plane = (size_t)H * W;
     for (int c = 0; c < 3; ++c) {
         double acc = 0.0;
         for (int j = 0; j < kk; ++j)
-            acc += w[j] * (double)radiance[c * plane + (size_t)qy[j] * W + qx[j]];
+            acc += w[j] * rad_at(radiance, c * plane + (size_t)qy[j] * W + qx[j]);
         R[c] = acc;
     }
 }
@@ -153,7 +170,7 @@ int kmdo_apply(const double* kmap, int32_t k, const float* radiance,
         for (int x = 0; x < W; ++x) {
             double R[3];
             window_taps(H, W, k, y, x, qy, qx);      /* the q_j of Step 1 */
-            apply_window(kmap + ((size_t)y * W + x) * kk, qy, qx, kk, radiance, H, W, R);
+            apply_window(kmap + ((size_t)y * W + x) * kk, qy, qx, kk, rad_f32(radiance), H, W, R);
             for (int c = 0; c < 3; ++c) out[c * plane + (size_t)y * W + x] = R[c];
         }
     free(qy); free(qx);
@@ -181,7 +198,7 @@ int kmdo_fuse(const double* filtered, const float* blend, int32_t M,
 
 /* ===================== streaming (per-pixel) entry points ================ */
 
-static int check_all(const float* radiance, const float* importance, const float* blend,
+static int check_all(const void* radiance, const float* importance, const float* blend,
                      int32_t N, int32_t H, int32_t W, int32_t M, const int32_t* sizes) {
     if (!radiance || !importance || !sizes) return KMDO_ERR_NULL;
     if (M < 1 || M > 64) return KMDO_ERR_CONFIG;
@@ -216,7 +233,7 @@ static void scratch_free(scratch_t* s) {
 }
 
 /* One output pixel: Steps 1-4 in the paper's order, for each size k_i. */
-static void pixel(const float* radiance, const float* importance, const float* blend,
+static void pixel(rad_t radiance, const float* importance, const float* blend,
                   int H, int W, int M, const int32_t* sizes, int blend_is_logits,
                   int n, int y, int x, scratch_t* s, double out[3]) {
     const size_t plane = (size_t)H * W;
@@ -225,7 +242,7 @@ static void pixel(const float* radiance, const float* importance, const float* b
         const float* Ii = importance + ((size_t)n * M + i) * plane;
         unfold_pixel(Ii, H, W, k, y, x, s->u, s->qy, s->qx);          /* Fig. 3  */
         softmax_window(s->u, kk, s->w);                                /* Eq. 3   */
-        apply_window(s->w, s->qy, s->qx, kk, radiance + (size_t)n * 3 * plane,
+        apply_window(s->w, s->qy, s->qx, kk, rad_offset(radiance, (size_t)n * 3 * plane),
                      H, W, s->Ri + 3 * i);                             /* Eq. 4   */
     }
     double b[64];
@@ -234,13 +251,14 @@ static void pixel(const float* radiance, const float* importance, const float* b
     fuse_pixel(s->Ri, b, M, blend_is_logits, out);                     /* Eq. 5   */
 }
 
-int kmdo_decode_filter_fuse_rows(const float* radiance, const float* importance,
-                                 const float* blend, int32_t N, int32_t H, int32_t W,
-                                 int32_t M, const int32_t* sizes, int32_t blend_is_logits,
-                                 int32_t y_begin, int32_t y_end, int32_t threads,
-                                 double* out) {
+static int rows_impl(rad_t radiance, const float* importance,
+                     const float* blend, int32_t N, int32_t H, int32_t W,
+                     int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                     int32_t y_begin, int32_t y_end, int32_t threads,
+                     double* out) {
     if (!out) return KMDO_ERR_NULL;
-    int st = check_all(radiance, importance, blend, N, H, W, M, sizes);
+    int st = check_all(radiance.f ? (const void*)radiance.f : (const void*)radiance.d, importance, blend, N, H, W,
+                       M, sizes);
     if (st) return st;
     if (y_begin < 0 || y_end > H || y_begin > y_end) return KMDO_ERR_DIM;
     const int rows = y_end - y_begin;
@@ -278,12 +296,31 @@ int kmdo_decode_filter_fuse_rows(const float* radiance, const float* importance,
     return err;
 }
 
+int kmdo_decode_filter_fuse_rows(const float* radiance, const float* importance,
+                                 const float* blend, int32_t N, int32_t H, int32_t W,
+                                 int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                                 int32_t y_begin, int32_t y_end, int32_t threads,
+                                 double* out) {
+    rad_t r = {radiance, NULL};
+    return rows_impl(r, importance, blend, N, H, W, M, sizes, blend_is_logits, y_begin, y_end, threads, out);
+}
+
+int kmdo_decode_filter_fuse_rows_f64rad(const double* radiance, const float* importance,
+                                        const float* blend, int32_t N, int32_t H, int32_t W,
+                                        int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                                        int32_t y_begin, int32_t y_end, int32_t threads,
+                                        double* out) {
+    rad_t r = {NULL, radiance};
+    return rows_impl(r, importance, blend, N, H, W, M, sizes, blend_is_logits, y_begin, y_end, threads, out);
+}
+
 int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importance,
                                    const float* blend, int32_t N, int32_t H, int32_t W,
                                    int32_t M, const int32_t* sizes, int32_t blend_is_logits,
                                    const int32_t* n, const int32_t* y, const int32_t* x,
                                    int64_t count, int32_t threads, double* out) {
     if (!out || !n || !y || !x) return KMDO_ERR_NULL;
+    const rad_t rf = {radiance, NULL};
     int st = check_all(radiance, importance, blend, N, H, W, M, sizes);
     if (st) return st;
     for (int64_t t = 0; t < count; ++t)
@@ -307,7 +344,7 @@ int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importanc
 #pragma omp for schedule(dynamic, 64)
 #endif
             for (int64_t t = 0; t < count; ++t)
-                pixel(radiance, importance, blend, H, W, M, sizes, blend_is_logits,
+                pixel(rf, importance, blend, H, W, M, sizes, blend_is_logits,
                       n[t], y[t], x[t], &s, out + 3 * t);
         }
         scratch_free(&s);
@@ -419,7 +456,7 @@ int kmdo_backward(const float* radiance, const float* importance, const float* b
                     const float* Ii = importance + ((size_t)n * M + i) * plane;
                     unfold_pixel(Ii, H, W, k, y, x, s.u, qyall + i * kkmax, qxall + i * kkmax);
                     softmax_window(s.u, kk, wall + i * kkmax);
-                    apply_window(wall + i * kkmax, qyall + i * kkmax, qxall + i * kkmax, kk, rad, H, W,
+                    apply_window(wall + i * kkmax, qyall + i * kkmax, qxall + i * kkmax, kk, rad_f32(rad), H, W,
                                  s.Ri + 3 * i);
                 }
                 /* Step 4 weights */

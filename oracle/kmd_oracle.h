@@ -77,6 +77,13 @@ int kmdo_decode_filter_fuse_rows(const float* radiance, const float* importance,
 
 /* Same, for an explicit list of pixels (frame n[t], row y[t], column x[t]);
  * out[t*3 + c].  Used to check sampled outputs of full-size frames. */
+/* The same with the radiance in fp64 (the multi-resolution oracle filters
+ * its fp64 pyramid levels D^l(r) without rounding them). */
+int kmdo_decode_filter_fuse_rows_f64rad(const double* radiance, const float* importance,
+                                        const float* blend, int32_t N, int32_t H, int32_t W,
+                                        int32_t M, const int32_t* sizes, int32_t blend_is_logits,
+                                        int32_t y_begin, int32_t y_end, int32_t threads,
+                                        double* out);
 int kmdo_decode_filter_fuse_pixels(const float* radiance, const float* importance,
                                    const float* blend, int32_t N, int32_t H, int32_t W,
                                    int32_t M, const int32_t* sizes, int32_t blend_is_logits,

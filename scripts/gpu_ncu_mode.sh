@@ -4,7 +4,7 @@ MODE=$1; TAG=$2
 cd $GRAFT_REPO_ROOT
 case $MODE in
   bwd) K='regex:lse_kernel|fused_tma|bwd_'; N=4 ;;
-  mr) K='regex:down4|fused_tma|combine'; N=6 ;;
+  mr) K='regex:down4|fused_tma|combine'; N=4 ;;
   temporal) K='regex:temporal'; N=1 ;;
 esac
 CMD="python bench.py --mode $MODE --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 0"

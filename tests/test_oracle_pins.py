@@ -426,7 +426,7 @@ def test_mr_three_levels_constant_radiance_exact(oracle_mod):
 def test_mr_two_levels_uniform_importance_is_scipy_pyramid(oracle_mod):
     # Uniform importance turns every level into a clamp-to-edge box mean
     # (pinned above), so a two-level M = 1 "Ours MR" is, written with scipy and
-    # numpy only: f = box_3(r), c = box_5(fp32(D r)) (R19), o = f + a (U c - U D f)
+    # numpy only: f = box_3(r), c = box_5(D r) (D r in fp64), o = f + a (U c - U D f)
     H, W = 12, 20
     rad = RNG.exponential(1.0, (1, 3, H, W)).astype(np.float32)
     imps = [np.zeros((1, 1, H, W), np.float32), np.zeros((1, 1, H // 2, W // 2), np.float32)]
@@ -441,7 +441,7 @@ def test_mr_two_levels_uniform_importance_is_scipy_pyramid(oracle_mod):
 
     r64 = rad.astype(np.float64)
     f = np.stack([_box(r64[0, c], 3) for c in range(3)])[None]
-    dr = D(r64).astype(np.float32).astype(np.float64)
+    dr = D(r64)
     cc = np.stack([_box(dr[0, c], 5) for c in range(3)])[None]
     ref = f + alpha.astype(np.float64) * (U(cc) - U(D(f)))
     np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
@@ -677,3 +677,38 @@ def test_temporal_reduces_variance_static_scene(oracle_mod):
                                                 pos_tol=0.1, alpha=0.2)
     v = acc.var()
     assert v < 0.2 and abs(acc.mean() - c) < 0.05
+
+
+# ----------------------------------------- Eq. 5 through the kmdo_fuse entry point
+def test_fuse_entry_point_special_cases(oracle_mod):
+    # kmdo_fuse itself (not via decode_filter_fuse): M = 1 is the identity
+    # (SPEC.md:275), equal logits give the arithmetic mean, a
+    # logit 40 above the others selects its input, and adding a
+    # constant to every logit changes nothing.  Inputs differ per
+    # (size, channel, pixel) so a wrong index pairs the wrong values.
+    M, H, W = 4, 5, 7
+    filt = RNG.uniform(0.1, 10.0, (M, 3, H, W))
+    np.testing.assert_array_equal(oracle_mod.fuse(filt[:1], None), filt[0])
+    np.testing.assert_allclose(oracle_mod.fuse(filt, np.full((M, H, W), 1.25, np.float32)),
+                               filt.mean(axis=0), rtol=1e-14)
+    for i in range(M):
+        b = np.zeros((M, H, W), np.float32)
+        b[i] = 40.0
+        np.testing.assert_allclose(oracle_mod.fuse(filt, b), filt[i], rtol=1e-15)  # other weights ~ e^-40
+    logits = RNG.standard_normal((M, H, W)).astype(np.float32)
+    np.testing.assert_allclose(oracle_mod.fuse(filt, logits + np.float32(16.0)), oracle_mod.fuse(filt, logits),
+                               rtol=1e-6)
+    # alpha given (blend_is_logits=0): the weighted sum with the given weights
+    a = RNG.uniform(0, 1, (M, H, W)).astype(np.float32)
+    ref = (a.astype(np.float64)[:, None] * filt).sum(axis=0)
+    np.testing.assert_allclose(oracle_mod.fuse(filt, a, blend_is_logits=False), ref, rtol=1e-14)
+
+
+def test_f64_radiance_entry_point_matches_fp32_entry(oracle_mod):
+    # the multi-resolution oracle filters fp64 pyramid levels through
+    # kmdo_decode_filter_fuse_rows_f64rad: on fp32-representable values it must
+    # return exactly what the fp32 entry point returns
+    rad, imp, blend = _rand_inputs(9, 12, 2, RNG)
+    a = oracle_mod.decode_filter_fuse(rad, imp, blend, [3, 5])
+    b = oracle_mod.decode_filter_fuse(rad.astype(np.float64), imp, blend, [3, 5])
+    np.testing.assert_array_equal(a, b)
