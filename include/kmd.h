@@ -305,9 +305,12 @@ kmd_status kmd_combine_resolutions(const float* fine, const float* coarse, const
  *   grad_importance [N,M,H,W] = dL/dI_i,  grad_blend [N,M,H,W] = dL/dB_i
  *   (dL/dalpha_i when blend_is_logits == 0; may be NULL; zeros when M == 1).
  * The radiance gradient is not computed (rendered data).
- * Importance must lie in (-80, 80) (unshifted exp).  With a device workspace
+ * Every size must be <= 13 (else KMD_ERR_CONFIG).  Importance must lie in
+ * (-80, 80): the backward evaluates exp(I) unshifted and has no exact
+ * fallback, so values outside give inf / NaN gradients.  With a device workspace
  * of kmd_backward_workspace_bytes(...) bytes (8 M + 4 B per pixel: the
- * per-size pair s_i = a_i / den_i, d_i = G.R_i, and log sum_i exp(B_i)), W % 4 == 0, k <= 13 and 16-byte aligned buffers the
+ * per-size pair s_i = a_i / den_i, d_i = G.R_i, and log sum_i exp(B_i)), W % 4 == 0 and 16-byte aligned buffers
+ * (grad_importance included) the
  * TMA passes run (kmd_last_kernel() == 11); otherwise (or with workspace ==
  * NULL) a one-launch tiled kernel that needs no workspace (== 10).          */
 size_t kmd_backward_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg);

@@ -778,10 +778,16 @@ kmd_status kmd_decode_filter_fuse_backward(const float* radiance, const float* i
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
     if (workspace_bytes < kmd_backward_workspace_bytes(N, H, W, cfg))
         return fail(KMD_ERR_DIM, "workspace too small");
+    for (int i = 0; i < cfg->num_sizes; ++i)
+        if (cfg->sizes[i] > 13)
+            return fail(KMD_ERR_CONFIG, "backward: sizes[%d]=%d > 13 (both backward kernels stage r_max <= 6 halos)",
+                        i, cfg->sizes[i]);
     const int M = cfg->num_sizes;
     cudaError_t e;
+    // the TMA path stores dL/dI through a tensor map: grad_importance must be
+    // 16-byte aligned as well (else the one-launch kernel runs)
     if (workspace && kmd::bwd_tma_supported(H, W, M, cfg->sizes, radiance, importance, grad_out, workspace) &&
-        (M == 1 || ((uintptr_t)blend & 15) == 0)) {
+        ((uintptr_t)grad_importance & 15) == 0 && (M == 1 || ((uintptr_t)blend & 15) == 0)) {
         kmd::set_last_kernel(kmd::LK_BWD_TMA);
         e = kmd::launch_backward_tma(radiance, importance, M > 1 ? blend : nullptr, grad_out, grad_importance,
                                      grad_blend, N, H, W, M, cfg->sizes, cfg->blend_is_logits, workspace,

@@ -40,8 +40,6 @@ constexpr int SEG = 7, NSEG = 8;
 constexpr int NH = 2, NB = 2, NV = 3;
 constexpr int NFIELD = 4, NFUSE = (TH * NSEG + 31) / 32;  // 7
 constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
-constexpr float L2E = 1.44269502162933349609375f;
-constexpr float LN2_HI = 0.693147182464599609375f;
 
 // boxes: rows y0-6 .. y0+32, columns x0-8 .. x0+59, zero outside the frame
 struct alignas(128) SDSlot {
@@ -78,30 +76,6 @@ struct BParams {
     int debug;           // development switches (env KMD_DEBUG): 1 = no gI stores
 };
 
-__device__ __forceinline__ float exp_acc(float x) {  // as kmd_tma.cu
-    const float t = x * L2E;
-    const float r = fmaf(-t, LN2_HI, x);
-    const float e = ex2_approx(t);
-    return fmaf(e, r, e);
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
 
 __device__ __forceinline__ float4 fma4(float m, float4 a, float4 v) {

@@ -2,6 +2,7 @@
 // libkmd (product path; no oracle code is included or linked here).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -213,4 +214,50 @@ __device__ __forceinline__ void tmem_ld3(unsigned taddr, float4& v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(v.z) : "r"(taddr + 2) : "memory");
 }
 __device__ __forceinline__ void tmem_reg_fence3(float4& v) { asm volatile("" : "+f"(v.x), "+f"(v.y), "+f"(v.z)); }
+}  // namespace kmd
+
+// ---- TMA (cp.async.bulk.tensor), bulk-group waits and the exp of the box
+// sums: shared by the pipelined kernels (kmd_tma.cu, kmd_bwd_tma.cu)
+namespace kmd {
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+// L2 prefetch of a box (cp.async.bulk.prefetch.tensor): fire and forget
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
+// exp(x) = 2^t (1 + r) with t = fl(x log2 e) and r = x - t ln 2 (one FMA with
+// ln 2 rounded to fp32: the dropped t (ln 2 - fl(ln 2)) is below |t| 2^-28), to
+// first order in |r| <= 2^-24 |t| ln 2.  MUFU.EX2 + 3 FP32 ops; with an exact
+// 2^t this is <= 2.5 ulp for |x| <= 16 and <= 6 ulp at |x| = 88, plus
+// ex2.approx's own ~2 ulp (the two-constant Cody-Waite form
+// measured 2.6% slower for < 2e-7 of relative accuracy).
+constexpr float LN2_HI = 0.693147182464599609375f;           // fl(ln 2)
+__device__ __forceinline__ float exp_acc(float x) {
+    const float t = x * L2E;
+    const float r = fmaf(-t, LN2_HI, x);
+    const float e = ex2_approx(t);
+    return fmaf(e, r, e);
+}
+
 }  // namespace kmd

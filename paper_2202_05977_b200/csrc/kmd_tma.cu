@@ -173,7 +173,6 @@ constexpr int NTHREADS = (1 + NFIELD + NFUSE) * 32;
 constexpr int TMA_WARP = KMD_ROLE_ORDER ? NFUSE + NFIELD : 0;
 constexpr int FIELD_W0 = KMD_ROLE_ORDER ? NFUSE : 1;
 constexpr int FUSE_W0 = KMD_ROLE_ORDER ? 0 : 1 + NFIELD;
-constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 
 // Importance maps and fusion logits arrive as fp32, or as bf16 (NEXT row 4's
 // alternative: the network's low-precision output) -- IN16 below.  A bf16 row
@@ -306,47 +305,7 @@ __device__ unsigned long long g_instr[160 * 16 * INSTR_TAGS];
 #endif
 
 // ------------------------------------------------------------------ TMA PTX
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-// L2 prefetch of a box (cp.async.bulk.prefetch.tensor): fire and forget
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(x), "r"(y), "r"(z)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fuse_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NFUSE * 32) : "memory"); }
-
-// exp(x) = 2^t (1 + r) with t = fl(x log2 e) and r = x - t ln 2 (one FMA with
-// ln 2 rounded to fp32: the dropped t (ln 2 - fl(ln 2)) is below |t| 2^-28), to
-// first order in |r| <= 2^-24 |t| ln 2.  MUFU.EX2 + 3 FP32 ops; with an exact
-// 2^t this is <= 2.5 ulp for |x| <= 16 and <= 6 ulp at |x| = 88, plus
-// ex2.approx's own ~2 ulp (the two-constant Cody-Waite form
-// measured 2.6% slower for < 2e-7 of relative accuracy).
-constexpr float LN2_HI = 0.693147182464599609375f;           // fl(ln 2)
-__device__ __forceinline__ float exp_acc(float x) {
-    const float t = x * L2E;
-    const float r = fmaf(-t, LN2_HI, x);
-    const float e = ex2_approx(t);
-    return fmaf(e, r, e);
-}
 
 // Gil-Werman line sums (gw_line, gw_line_field): kmd_gw.cuh
 
@@ -363,6 +322,31 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
     c.x0 = (r - ty * tiles_x) * TW;
     c.y0 = ty < p.tile_rows_a ? p.tile_y_begin + ty * TH : p.tile_y_begin_b + (ty - p.tile_rows_a) * TH;
     return c;
+}
+
+// Border rows (clamp-to-edge, reading R1): read through a clamped row index by
+// a second, border-tile instantiation of the field loop (KMD_CLAMP_VARIANT 1,
+// default: no generic writes to the TMA boxes), or replicated into the boxes
+// by the field job (0: fix_rows, one code path).  The variant doubles the
+// field code (0.82 vs 0.42 no-instruction stall cycles per issued
+// instruction) yet measured faster: 56.2 vs 57.4 us per 1080p frame.
+#ifndef KMD_CLAMP_VARIANT
+#define KMD_CLAMP_VARIANT 1
+#endif
+constexpr bool CLAMP_VARIANT = KMD_CLAMP_VARIANT;
+template <int STRIDE = BW, class T>
+__device__ __forceinline__ void fix_rows(T* col, int plane_stride, int nplanes, int top, int bot) {
+    for (int pl = 0; pl < nplanes; ++pl) {
+        T* c = col + pl * plane_stride;
+        if (top > 0) {
+            const T v = c[top * STRIDE];
+            for (int r = 0; r < top; ++r) c[r * STRIDE] = v;
+        }
+        if (bot < FH) {
+            const T v = c[(bot - 1) * STRIDE];
+            for (int r = bot; r < FH; ++r) c[r * STRIDE] = v;
+        }
+    }
 }
 
 // ------------------------------------------------------------ field warps
@@ -514,10 +498,12 @@ __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alph
     } else {  // alpha given (blend_is_logits == 0)
         w = a * rden;
     }
-    const float2 a01 = __ffma2_rn(make_float2(w, w), make_float2(v.y, v.z), make_float2(st.a[j][0], st.a[j][1]));
-    st.a[j][0] = a01.x;
-    st.a[j][1] = a01.y;
-    st.a[j][2] = fmaf(w, v.w, st.a[j][2]);
+    // (v.z, v.w) is an aligned register pair of the LDS.128 quad: one FFMA2
+    // (pairing (v.y, v.z) instead costs two MOVs per pixel)
+    st.a[j][0] = fmaf(w, v.y, st.a[j][0]);
+    const float2 a12 = __ffma2_rn(make_float2(w, w), make_float2(v.z, v.w), make_float2(st.a[j][1], st.a[j][2]));
+    st.a[j][1] = a12.x;
+    st.a[j][2] = a12.y;
 }
 
 template <int MODE, class T>
@@ -821,8 +807,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
                 IWAIT(4, mbar_wait(EPRE ? &sm.e_full[si] : &sm.in_full[si], (seq / NI) & 1));
                 const int R = (rpack >> (4 * i)) & 15;
-                if (top > 0 || bot < FH) field_dispatch<true, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
-                else field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                if (KMD_DBG(32)) {
+                    // role isolation: no field arithmetic
+                } else if (CLAMP_VARIANT) {
+                    if (top > 0 || bot < FH) field_dispatch<true, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                    else field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                } else {
+                    if (top > 0 || bot < FH) {
+                        // rows of the boxes outside the frame / buffer take the nearest
+                        // valid row (R1), written into this job's columns; two jobs of a
+                        // tile may write the same radiance values (identical data)
+                        fix_rows<InElem<SP::IN16>::IW>(&in.I[0][ci], 1, 1, top, bot);
+                        if (!TMEM_RAD) fix_rows(&sm.rad[rb].v[0][0][cc], FH * BW, 3, top, bot);
+                        fence_proxy_async();  // generic writes before the slots' next TMA overwrite
+                        __syncwarp();
+                    }
+                    field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                }
                 // one arrive per warp: __syncwarp orders every lane's shared
                 // memory accesses before the elected lane's release-arrive
                 __syncwarp();

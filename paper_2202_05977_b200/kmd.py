@@ -164,12 +164,41 @@ def _dev_f32(name: str, t: torch.Tensor, shape=None, dtype=torch.float32) -> int
     return t.data_ptr()
 
 
+def _on_one_device(fn):
+    """Every tensor argument of a libkmd call must live on one CUDA device; the
+    call runs with that device current (libkmd queries the current device for
+    its SM count, function attributes and helper streams)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        devs = set()
+
+        def visit(v):
+            if isinstance(v, torch.Tensor):
+                if v.device.type == "cuda":
+                    devs.add(v.device)
+            elif isinstance(v, (list, tuple)):
+                for u in v:
+                    visit(u)
+        for v in list(args) + list(kwargs.values()):
+            visit(v)
+        if len(devs) > 1:
+            raise ValueError(f"{fn.__name__}: tensors on several devices {sorted(map(str, devs))}")
+        if not devs:
+            return fn(*args, **kwargs)
+        with torch.cuda.device(devs.pop()):
+            return fn(*args, **kwargs)
+    return wrapped
+
+
 def _stream(t: torch.Tensor, stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream(t.device)
     return stream.cuda_stream
 
 
+@_on_one_device
 def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
                        blend: Optional[torch.Tensor], sizes: Sequence[int],
                        out: Optional[torch.Tensor] = None, blend_is_logits: bool = True,
@@ -206,6 +235,7 @@ def decode_filter_fuse(radiance: torch.Tensor, importance: torch.Tensor,
     return out
 
 
+@_on_one_device
 def demodulate(radiance: torch.Tensor, albedo: torch.Tensor, eps: float = 1e-3,
                out: Optional[torch.Tensor] = None,
                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -220,6 +250,7 @@ def demodulate(radiance: torch.Tensor, albedo: torch.Tensor, eps: float = 1e-3,
     return out
 
 
+@_on_one_device
 def remodulate(irradiance: torch.Tensor, albedo: torch.Tensor, out: Optional[torch.Tensor] = None,
                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """out = irradiance * albedo (SPEC.md:138-145), [N,3,H,W] CUDA."""
@@ -233,6 +264,7 @@ def remodulate(irradiance: torch.Tensor, albedo: torch.Tensor, out: Optional[tor
     return out
 
 
+@_on_one_device
 def decode_filter(radiance: torch.Tensor, importance_i: torch.Tensor, k: int,
                   out: Optional[torch.Tensor] = None,
                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -247,6 +279,7 @@ def decode_filter(radiance: torch.Tensor, importance_i: torch.Tensor, k: int,
     return out
 
 
+@_on_one_device
 def fuse(filtered: torch.Tensor, blend: Optional[torch.Tensor], blend_is_logits: bool = True,
          out: Optional[torch.Tensor] = None,
          stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -262,6 +295,7 @@ def fuse(filtered: torch.Tensor, blend: Optional[torch.Tensor], blend_is_logits:
     return out
 
 
+@_on_one_device
 def decode_filter_fuse_band(radiance: torch.Tensor, importance: torch.Tensor,
                             blend: Optional[torch.Tensor], sizes: Sequence[int], *,
                             y0: int, band_rows: int, halo_top: int, halo_bot: int,
@@ -290,6 +324,7 @@ def decode_filter_fuse_band(radiance: torch.Tensor, importance: torch.Tensor,
 BAND_ALL, BAND_INTERIOR, BAND_SEAMS = 0, 1, 2
 
 
+@_on_one_device
 def decode_filter_fuse_band_part(radiance: torch.Tensor, importance: torch.Tensor,
                                  blend: Optional[torch.Tensor], sizes: Sequence[int], part: int, *,
                                  y0: int, band_rows: int, halo_top: int, halo_bot: int, H_global: int,
@@ -335,6 +370,7 @@ class Comm:
             self.handle = ctypes.c_void_p()
 
 
+@_on_one_device
 def halo_exchange(comm: Comm, planes: Sequence[torch.Tensor], band_rows: int, halo: int,
                   peer_up: int, peer_down: int, stream: Optional[torch.cuda.Stream] = None) -> None:
     """kmd_halo_exchange over contiguous [halo_top + band_rows + halo_bot, W] CUDA planes."""
@@ -346,6 +382,7 @@ def halo_exchange(comm: Comm, planes: Sequence[torch.Tensor], band_rows: int, ha
                                    peer_up, peer_down, _stream(planes[0], stream)))
 
 
+@_on_one_device
 def band_step(comm: Optional[Comm], radiance: torch.Tensor, importance: torch.Tensor,
               blend: Optional[torch.Tensor], sizes: Sequence[int], out: torch.Tensor, *,
               y0: int, band_rows: int, halo: int, peer_up: int, peer_down: int, H_global: int,
@@ -377,6 +414,7 @@ def host_workspace_bytes(N: int, H: int, W: int, sizes: Sequence[int]) -> int:
     return int(lib().kmd_host_workspace_bytes(N, H, W, ctypes.byref(cfg)))
 
 
+@_on_one_device
 def decode_filter_fuse_host(radiance: torch.Tensor, importance: torch.Tensor,
                             blend: Optional[torch.Tensor], sizes: Sequence[int],
                             out: torch.Tensor, workspace: torch.Tensor,
@@ -447,6 +485,7 @@ def mr_workspace_bytes(N: int, H: int, W: int, sizes_per_level) -> int:
     return int(lib().kmd_mr_workspace_bytes(N, H, W, ctypes.byref(cfg)))
 
 
+@_on_one_device
 def mr_decode_filter_fuse(radiance: torch.Tensor, importance, blend, alpha, sizes_per_level,
                           out: Optional[torch.Tensor] = None,
                           workspace: Optional[torch.Tensor] = None,
@@ -482,6 +521,7 @@ def mr_decode_filter_fuse(radiance: torch.Tensor, importance, blend, alpha, size
     return out
 
 
+@_on_one_device
 def downsample2x2(x: torch.Tensor, out: Optional[torch.Tensor] = None,
                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     N, C, H, W = x.shape
@@ -493,6 +533,7 @@ def downsample2x2(x: torch.Tensor, out: Optional[torch.Tensor] = None,
     return out
 
 
+@_on_one_device
 def combine_resolutions(fine: torch.Tensor, coarse: torch.Tensor, alpha: torch.Tensor,
                         out: Optional[torch.Tensor] = None,
                         stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -513,6 +554,7 @@ def backward_workspace_bytes(N: int, H: int, W: int, sizes: Sequence[int]) -> in
     return int(lib().kmd_backward_workspace_bytes(N, H, W, ctypes.byref(cfg)))
 
 
+@_on_one_device
 def decode_filter_fuse_backward(radiance: torch.Tensor, importance: torch.Tensor,
                                 blend: Optional[torch.Tensor], grad_out: torch.Tensor,
                                 sizes: Sequence[int], blend_is_logits: bool = True,
@@ -578,6 +620,7 @@ class DecodeFilterFuse(torch.autograd.Function):
 
 
 # ------------------------------------------------ temporal accumulation (NEXT row 4)
+@_on_one_device
 def temporal_accumulate(cur_rad: torch.Tensor, prev_rad: torch.Tensor, prev_pos: torch.Tensor,
                         prev_nrm: torch.Tensor, prev_valid: torch.Tensor, cur_pos: torch.Tensor,
                         cur_nrm: torch.Tensor, motion: torch.Tensor, pos_tol: float,

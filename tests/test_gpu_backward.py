@@ -131,3 +131,29 @@ def test_backward_540p_full_frame_tma(oracle_mod, cuda_device):
                                  G.numpy().astype(np.float64), PAPER)
     _normwise(gI.cpu().numpy(), rI, "540p grad_importance")
     _normwise(gB.cpu().numpy(), rB, "540p grad_blend")
+
+
+def test_backward_rejects_sizes_above_13(cuda_device):
+    inp = gen.make_inputs(1, 40, 48, 2, seed=3)
+    G = torch.randn((1, 3, 40, 48), device=cuda_device)
+    with pytest.raises(kmd.KmdError, match="CONFIG"):
+        kmd.decode_filter_fuse_backward(inp.radiance.to(cuda_device), inp.importance.to(cuda_device),
+                                        inp.blend.to(cuda_device), G, [3, 15])
+
+
+def test_backward_unaligned_grad_importance_takes_the_tiled_kernel(oracle_mod, cuda_device):
+    # grad_importance 4 bytes past a 16-byte boundary: the TMA path cannot store
+    # through a tensor map, so the one-launch kernel runs (and is correct)
+    N, H, W, sizes = 1, 40, 64, [3, 5]
+    inp = gen.make_inputs(N, H, W, 2, seed=5)
+    G = torch.randn((N, 3, H, W), generator=torch.Generator().manual_seed(1))
+    flat = torch.empty(N * 2 * H * W + 1, device=cuda_device)
+    gi = flat[1:].view(N, 2, H, W)
+    ws = torch.empty(kmd.backward_workspace_bytes(N, H, W, sizes), dtype=torch.uint8, device=cuda_device)
+    kmd.decode_filter_fuse_backward(inp.radiance.to(cuda_device), inp.importance.to(cuda_device),
+                                    inp.blend.to(cuda_device), G.to(cuda_device), sizes, grad_importance=gi,
+                                    workspace=ws)
+    torch.cuda.synchronize()
+    assert kmd.last_kernel() == "bwd-tile"
+    ri, _ = oracle_mod.backward(inp.radiance.numpy(), inp.importance.numpy(), inp.blend.numpy(), G.numpy(), sizes)
+    _normwise(gi.cpu().numpy(), ri, "unaligned grad_importance")
