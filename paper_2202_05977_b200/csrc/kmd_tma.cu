@@ -70,6 +70,7 @@ static_assert(FW == 64, "two 32-lane field halves per size");
 #ifndef KMD_TH
 #define KMD_TH 27
 #endif
+#define KMD_TH_VALUE KMD_TH
 constexpr int TH = KMD_TH;          // output rows per tile
 constexpr int FH = TH + 2 * RMAX;   // 39 field rows in every box
 // Every TMA box starts at column x0-8: the innermost box coordinate must be a
@@ -138,6 +139,15 @@ constexpr int NRAD = TMEM_RAD ? 1 : 2;  // radiance boxes in shared memory
 #define KMD_EPRE_AHEAD 2
 #endif
 constexpr int EPRE_AHEAD = KMD_EPRE_AHEAD;
+// exp(B_i) of each blend box computed in place by the field jobs of the same
+// step, before they release the step's V slot (KMD_BEXP 1), so that the
+// fusion warps read exp(B_i) directly.  Off: measured 61.6 vs 56.1 us with 4
+// field warps, and 57.0 vs 57.1 us with the vertical split (KMD_VSPLIT) --
+// the fusion warps are latency-bound, 20% fewer of their instructions buys
+// nothing.  (Compiled softmax specialisations with fp32 logits only.)
+#ifndef KMD_BEXP
+#define KMD_BEXP 0
+#endif
 // blend logits issued by a second producer lane (1) or by the importance
 // producer, in step order (0, default: measured 57.0 vs 58.6 us per 1080p frame)
 #ifndef KMD_BLANE
@@ -157,8 +167,23 @@ constexpr unsigned TMEM_COLS = 256; // 4 columns (r, g, b, -) per box row: 4 x 3
 // field warps; a field job is one (tile, size, 32-column half) walk, and the
 // jobs of consecutive tiles are dealt to the field warps round-robin in one
 // global sequence, so any NFIELD keeps every warp equally loaded
+// Vertical split of the field jobs (KMD_VSPLIT 1): a job is (tile, size,
+// 32-column half, vertical half), the top half producing V rows 0..13, the
+// bottom half rows 13..26 (row 13 stored by the top job only); each walk
+// recomputes 2R halo rows of the other half, and 8 field warps keep 2 sizes
+// in flight with half-length dependency chains (16 warps: 128 registers, no
+// spills).  Off: measured 57.1 vs 56.1 us.  With it the field warps wait
+// 35-50% of the time on free V slots while the fusion warps stay ~86% busy
+// (KMD_INSTR wait breakdown): the fusion role sets the pace.
+#ifndef KMD_VSPLIT
+#define KMD_VSPLIT 0
+#endif
+constexpr int NVH = KMD_VSPLIT ? 2 : 1;       // vertical halves per (size, column half)
+constexpr int VROWS = KMD_VSPLIT ? (KMD_TH_VALUE + 1) / 2 : KMD_TH_VALUE;  // V rows one job produces
+constexpr int JPS = 2 * NVH;                  // field jobs per (tile, size)
+static_assert(!KMD_TMEM_RAD || NVH == 1, "TMEM radiance keeps whole-column jobs");
 #ifndef KMD_NFIELD
-#define KMD_NFIELD 4
+#define KMD_NFIELD (KMD_VSPLIT ? 8 : 4)
 #endif
 constexpr int NFIELD = KMD_NFIELD;
 constexpr int NFUSE = (TH * NSEG + 31) / 32;  // fusion warps (one thread per (row, segment))
@@ -360,7 +385,10 @@ __device__ __forceinline__ void fix_rows(T* col, int plane_stride, int nplanes, 
 // (r, g, b) at columns 4f .. 4f+2.
 template <int R, bool CLAMP, bool EXPF, class SM, class IS>
 __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci, int top,
-                                          int bot, unsigned tm) {
+                                          int bot, unsigned tm, int vh) {
+    // vertical half vh (KMD_VSPLIT): V rows oy0 .. oy0 + VROWS - 1, of which
+    // the first `skip` belong to the top job
+    const int oy0 = vh ? TH - VROWS : 0, skip = vh ? 2 * VROWS - TH : 0;
     constexpr int IW = sizeof(in.I[0]) / sizeof(in.I[0][0]);
     const int c = h * 32 + (threadIdx.x & 31);
     KMD_CHECK(cc >= 0 && cc < BW && ci >= 0 && ci < IW && c < 64 && rb >= 0 && rb < NRAD);
@@ -372,8 +400,9 @@ __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb
         // to assemble a 16-byte quad); same 4 wavefronts per warp as STS.128
         // (one STS.128 would halve the store wavefronts but costs MOVs to
         // assemble the quad: measured 7% slower)
-        KMD_CHECK(oy >= 0 && oy < TH);
-        const unsigned a = smem_u32(&Vc[oy * VS]);
+        KMD_CHECK(oy >= 0 && oy0 + oy < TH);
+        if (NVH > 1 && oy < skip) return;
+        const unsigned a = smem_u32(&Vc[(oy0 + oy) * VS]);
         asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
         asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.z), "f"(v.w) : "memory");
     };
@@ -403,9 +432,9 @@ __device__ __forceinline__ void field_job(SM& sm, const IS& in, Slot& sl, int rb
             },
             emit);
     } else {
-        gw_line_field<R, TH>(
+        gw_line_field<R, VROWS>(
             [&](int f) {
-                const int row = CLAMP ? clampi(RMAX - R + f, top, bot - 1) : RMAX - R + f;
+                const int row = CLAMP ? clampi(RMAX - R + oy0 + f, top, bot - 1) : RMAX - R + oy0 + f;
                 KMD_CHECK(row >= 0 && row < FH);
                 const float v = ld_in(Ib + row * IW);
                 const float r = Rb[row * BW], g = Rb[FH * BW + row * BW], b = Rb[2 * FH * BW + row * BW];
@@ -439,15 +468,15 @@ __device__ __forceinline__ void rad_to_tmem(const RadBuf& rad, int cc, int top, 
 
 template <bool CLAMP, bool EXPF, class SM, class IS>
 __device__ __forceinline__ void field_dispatch(int R, SM& sm, const IS& in, Slot& sl, int rb, int h, int cc, int ci,
-                                               int top, int bot, unsigned tm) {
+                                               int top, int bot, unsigned tm, int vh) {
     switch (R) {
-        case 0: field_job<0, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 1: field_job<1, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 2: field_job<2, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 3: field_job<3, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 4: field_job<4, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        case 5: field_job<5, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
-        default: field_job<6, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm); break;
+        case 0: field_job<0, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        case 1: field_job<1, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        case 2: field_job<2, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        case 3: field_job<3, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        case 4: field_job<4, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        case 5: field_job<5, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
+        default: field_job<6, CLAMP, EXPF>(sm, in, sl, rb, h, cc, ci, top, bot, tm, vh); break;
     }
 }
 
@@ -480,7 +509,7 @@ struct Acc {
 // logit beyond the fp32 exp range (S = 0 or inf, non-finite acc) or a box
 // denominator outside [1e-30, 1e30] sends the pixel to the exact path (reading
 // R13).
-enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2, FUSE_BWD_H = 3 };
+enum { FUSE_ONE = 0, FUSE_SOFTMAX = 1, FUSE_ALPHA = 2, FUSE_BWD_H = 3, FUSE_SOFTMAX_PRE = 4 };
 
 template <int MODE>
 __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alpha */, float4 v) {
@@ -491,9 +520,9 @@ __device__ __forceinline__ void fuse_px(Acc& st, int j, float a /* logit or alph
     float w;
     if constexpr (MODE == FUSE_ONE) {
         w = rden;
-    } else if constexpr (MODE == FUSE_SOFTMAX) {
-        a = exp_acc(a);  // the blend logit -> exp(B_i), unshifted (reading R2)
-        st.S[j] += a;
+    } else if constexpr (MODE == FUSE_SOFTMAX || MODE == FUSE_SOFTMAX_PRE) {
+        if constexpr (MODE == FUSE_SOFTMAX) a = exp_acc(a);  // the blend logit -> exp(B_i), unshifted (reading R2)
+        st.S[j] += a;  // FUSE_SOFTMAX_PRE: the box already holds exp(B_i) (KMD_BEXP)
         w = a * rden;
     } else {  // alpha given (blend_is_logits == 0)
         w = a * rden;
@@ -652,6 +681,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int M = SP::M > 0 ? SP::M : p.M;
     constexpr bool EPRE = KMD_EPRE && !SP::IN16 && SP::MODE != FUSE_BWD_H && !TMEM_RAD;
+    constexpr bool BEXP = KMD_BEXP && !SP::IN16 && SP::MODE == FUSE_SOFTMAX;
     const bool has_blend = p.blend != nullptr && !(KMD_DBG(16));
     unsigned rpack = 0;  // radius of size i in bits 4i..4i+3
     for (int i = 0; i < M; ++i) rpack |= (unsigned)((p.sizes[i] - 1) / 2) << (4 * i);
@@ -664,10 +694,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int s = 0; s < NI; ++s) {
             mbar_init(&sm.in_full[s], 1);
             mbar_init(&sm.e_full[s], NFUSE);             // every fusion warp's share of exp(I) (EPRE)
-            mbar_init(&sm.in_empty[s], 2);              // both halves (one elected lane each)
+            mbar_init(&sm.in_empty[s], JPS);            // every field job of the step (one elected lane each)
         }
         for (int s = 0; s < NV; ++s) {
-            mbar_init(&sm.v_full[s], 2);                // both halves (one elected lane each)
+            mbar_init(&sm.v_full[s], JPS);              // every field job of the step (one elected lane each)
             mbar_init(&sm.v_empty[s], NFUSE);
         }
         for (int s = 0; s < NB; ++s) {
@@ -680,7 +710,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if constexpr (VS > 64) {
         // V columns past the 64 field columns: read (not stored) by the last
         // segment's recomputed pixels; keep them finite
-        constexpr int PADC = VS - 64;
+        constexpr int PADC = VS > 64 ? VS - 64 : 1;
         for (int k = threadIdx.x; k < NV * TH * PADC; k += NTHREADS)
             sm.slot[k / (TH * PADC)].V[(k / PADC) % TH][64 + k % PADC] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -776,12 +806,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // then runs its jobs of the tile.  A job waits for a free V slot and
         // its importance box, writes the vertical sums of its 32 columns and
         // releases the importance slot and the V slot (to the fusion warps).
-        static_assert(NFIELD % 2 == 0, "field warps keep one column half each");
+        static_assert(!TMEM_RAD || (NFIELD % 2 == 0 && NVH == 1), "TMEM radiance: field warps keep one column half");
         const int fw = warp - FIELD_W0;
-        const int h = fw & 1;
         const int ylo = max(0, p.row_base), yhi = min(p.H, p.row_base + p.buf_rows) - 1;
         const unsigned tm = TMEM_RAD ? sm.tmem_base + ((unsigned)(32 * (warp & 3)) << 16) : 0u;
-        const int c = h * 32 + lane;
         int g = fw;
         for (int tl = 0; tl < my_tiles; ++tl) {
             const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
@@ -789,13 +817,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl / NRAD) & 1));
             if constexpr (TMEM_RAD) {
                 const int top = max(0, ylo - (tc.y0 - RMAX)), bot = min(FH, yhi - (tc.y0 - RMAX) + 1);
+                const int c = (fw & 1) * 32 + lane;
                 rad_to_tmem(sm.rad[0], clampi(tc.x0 - RMAX + c, 0, p.W - 1) - (tc.x0 - XOFF), top, bot, tm);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.rad_empty[0]);
             }
 #pragma unroll 1
-            for (; g < 2 * M * (tl + 1); g += NFIELD) {
-                const int seq = g >> 1, i = seq - tl * M;
+            for (; g < JPS * M * (tl + 1); g += NFIELD) {
+                const int seq = g / JPS, i = seq - tl * M, jr = g - seq * JPS;
+                const int h = jr / NVH, vh = jr - h * NVH;  // column half, vertical half
+                const int c = h * 32 + lane;
                 // per job (short live ranges: the fusion role sets the register budget)
                 const int top = max(0, ylo - (tc.y0 - RMAX));           // box rows before the first valid row
                 const int bot = min(FH, yhi - (tc.y0 - RMAX) + 1);      // first box row after the last valid row
@@ -810,8 +841,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (KMD_DBG(32)) {
                     // role isolation: no field arithmetic
                 } else if (CLAMP_VARIANT) {
-                    if (top > 0 || bot < FH) field_dispatch<true, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
-                    else field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                    if (top > 0 || bot < FH) field_dispatch<true, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm, vh);
+                    else field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm, vh);
                 } else {
                     if (top > 0 || bot < FH) {
                         // rows of the boxes outside the frame / buffer take the nearest
@@ -822,7 +853,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         fence_proxy_async();  // generic writes before the slots' next TMA overwrite
                         __syncwarp();
                     }
-                    field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm);
+                    field_dispatch<false, !EPRE>(R, sm, in, sl, rb, h, cc, ci, top, bot, tm, vh);
+                }
+                if constexpr (BEXP) {
+                    if (has_blend) {
+                        // this job's share (float4s jr, jr + JPS, ... of the step's
+                        // blend box): B -> exp(B) in place, before the V slot (and
+                        // with it the box) goes to the fusion warps
+                        const int sb = seq % NB;
+                        IWAIT(5, mbar_wait(&sm.b_full[sb], (seq / NB) & 1));
+                        float4* b4 = reinterpret_cast<float4*>(&sm.bl[sb].B[0][0]);
+                        constexpr int NQ = TH * InElem<SP::IN16>::BBW / 4;
+#pragma unroll 1
+                        for (int k = jr * 32 + lane; k < NQ; k += JPS * 32) {
+                            float4 v = b4[k];
+                            v.x = exp_acc(v.x);
+                            v.y = exp_acc(v.y);
+                            v.z = exp_acc(v.z);
+                            v.w = exp_acc(v.w);
+                            b4[k] = v;
+                        }
+                        fence_proxy_async();  // generic writes before the slot's next TMA overwrite
+                    }
                 }
                 // one arrive per warp: __syncwarp orders every lane's shared
                 // memory accesses before the elected lane's release-arrive
@@ -1040,7 +1092,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 epre(tl * M + i + EPRE_AHEAD);
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                if (!(KMD_DBG(64)) && active) fuse_job<SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
+                if (!(KMD_DBG(64)) && active) fuse_job<BEXP ? FUSE_SOFTMAX_PRE : SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
                                                                    (rpack >> (4 * i)) & 15);
                 __syncwarp();
                 if ((c & 31) == 0) {
