@@ -1092,8 +1092,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 epre(tl * M + i + EPRE_AHEAD);
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
-                if (!(KMD_DBG(64)) && active) fuse_job<BEXP ? FUSE_SOFTMAX_PRE : SP::MODE>(p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
-                                                                   (rpack >> (4 * i)) & 15);
+                IWAIT(12, if (!(KMD_DBG(64)) && active) fuse_job<BEXP ? FUSE_SOFTMAX_PRE : SP::MODE>(
+                              p, sm.slot[vs], sm.bl[bs], st, ty, xs, xs + xalign<SP::IN16>(tc.x0),
+                              (rpack >> (4 * i)) & 15));
                 __syncwarp();
                 if ((c & 31) == 0) {
                     // the last size's slot becomes the stage: warp 0 withholds its arrival (pend)
@@ -1111,6 +1112,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 continue;
             }
             // ---- normalise, exact fallback for flagged pixels, stage, TMA store
+#ifdef KMD_INSTR
+            const long long t_epi = clock64();
+#endif
             IWAIT(9, fuse_bar());  // every fusion thread is done with the last V: it becomes the stage
             auto stage = stage_of(sm.slot[stage_slot]);
             const int gy = tc.y0 + ty;
@@ -1200,6 +1204,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 fuse_bar();  // every thread is done reading the stage slot
             }
             pend = stage_slot;  // released after the next tile's first size (or never: kernel end)
+#ifdef KMD_INSTR
+            instr[13] += (unsigned long long)(clock64() - t_epi);
+#endif
         }
         if (c == 0) bulk_wait0();
     }

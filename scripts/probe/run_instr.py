@@ -18,9 +18,10 @@ buf = np.zeros(n, dtype=np.uint64)
 L.kmd_debug_read_instr(buf.ctypes.data, n)
 a = buf.reshape(160, 16, 16)[:148].astype(np.float64)
 tags = ["rad_empty(TMA)", "in_empty(TMA)", "rad_full(F)", "v_empty(F)", "in_full(F)", "b_full(F)",
-        "v_full(U)", "b_full(U)", "b_empty(TMA)", "fusebar1(U)", "fusebar2(U)", "epre_in_full(U)"]
+        "v_full(U)", "b_full(U)", "b_empty(TMA)", "fusebar1(U)", "fusebar2(U)", "epre_in_full(U)",
+        "fuse_job(U)", "epilogue(U)"]
 nw = int(os.environ.get("NWARPS", "11"))
 for w in range(nw):
     tot = a[:, w, 15].mean()
-    parts = ", ".join(f"{tags[t]}={a[:, w, t].mean() / tot:.0%}" for t in range(12) if a[:, w, t].mean() > 0)
+    parts = ", ".join(f"{tags[t]}={a[:, w, t].mean() / tot:.0%}" for t in range(14) if a[:, w, t].mean() > 0)
     print(f"warp {w:2d}: total {tot / 1.9e3:.1f} us-equiv  waits: {parts}")
