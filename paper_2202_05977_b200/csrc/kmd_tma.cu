@@ -148,6 +148,12 @@ constexpr int EPRE_AHEAD = KMD_EPRE_AHEAD;
 #ifndef KMD_BEXP
 #define KMD_BEXP 0
 #endif
+// fusion warps of odd index process each pair of sizes in swapped order
+// (KMD_STAGGER 1): spreads the V-load bursts of a step over time
+#ifndef KMD_STAGGER
+#define KMD_STAGGER 0
+#endif
+constexpr bool STAGGER = KMD_STAGGER;
 // blend logits issued by a second producer lane (1) or by the importance
 // producer, in step order (0, default: measured 57.0 vs 58.6 us per 1080p frame)
 #ifndef KMD_BLANE
@@ -551,9 +557,36 @@ __device__ __forceinline__ void hbox(const Slot& sl, int ty, int xs, float4 (&o)
     gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { o[x] = v; });
 }
 
+// HFUSE: the horizontal sums of one radius emitted straight into the fusion
+// arithmetic (no o[SEG] array: fewer live registers, the fusion code once per
+// radius)
+template <int R, int MODE, class T>
+__device__ __forceinline__ void hfuse(const Slot& sl, int ty, int xs, const T* Br, Acc& st) {
+    KMD_CHECK(ty >= 0 && ty < TH && xs + RMAX - R >= 0 && xs + RMAX + R + SEG <= VS);
+    const float4* Vr = &sl.V[ty][xs + RMAX - R];
+    gw_line<R, SEG>([&](int j) { return Vr[j]; }, [&](int x, float4 v) { fuse_px<MODE>(st, x, ld_in(Br + x), v); });
+}
+#ifndef KMD_HFUSE
+#define KMD_HFUSE 0
+#endif
+
 template <int SMODE, class BS>
 __device__ __forceinline__ void fuse_job(const FusedParams& p, const Slot& sl, const BS& bs, Acc& st, int ty,
                                          int xs, int xb, int R) {
+    if constexpr (KMD_HFUSE && SMODE >= 0) {
+        KMD_CHECK(xb >= 0 && xb + SEG <= (int)(sizeof(bs.B[0]) / sizeof(bs.B[0][0])));
+        const auto* Br = &bs.B[ty][xb];
+        switch (R) {
+            case 0: hfuse<0, SMODE>(sl, ty, xs, Br, st); break;
+            case 1: hfuse<1, SMODE>(sl, ty, xs, Br, st); break;
+            case 2: hfuse<2, SMODE>(sl, ty, xs, Br, st); break;
+            case 3: hfuse<3, SMODE>(sl, ty, xs, Br, st); break;
+            case 4: hfuse<4, SMODE>(sl, ty, xs, Br, st); break;
+            case 5: hfuse<5, SMODE>(sl, ty, xs, Br, st); break;
+            default: hfuse<6, SMODE>(sl, ty, xs, Br, st); break;
+        }
+        return;
+    }
     float4 o[SEG];
     switch (R) {
         case 0: hbox<0>(sl, ty, xs, o); break;
@@ -1088,8 +1121,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 st.dmin[j] = INFINITY;
             }
 #pragma unroll 1
-            for (int i = 0; i < M; ++i) {
-                epre(tl * M + i + EPRE_AHEAD);
+            for (int ii = 0; ii < M; ++ii) {
+                // STAGGER: the odd fusion warps take the sizes of each pair in
+                // swapped order, so the fusion warps' V loads of a step do not all
+                // hit the shared-memory pipe at once
+                const int i = (STAGGER && ((c >> 5) & 1) && (ii ^ 1) < M) ? (ii ^ 1) : ii;
+                const int seq = tl * M + i;
+                if (STAGGER) {
+                    vs = seq % NV; vph = (seq / NV) & 1;
+                    bs = seq % NB; bph = (seq / NB) & 1;
+                }
+                epre(tl * M + ii + EPRE_AHEAD);
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
                 IWAIT(12, if (!(KMD_DBG(64)) && active) fuse_job<BEXP ? FUSE_SOFTMAX_PRE : SP::MODE>(
@@ -1101,11 +1143,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (!(c == 0 && i == M - 1)) mbar_arrive(&sm.v_empty[vs]);
                     if (has_blend) mbar_arrive(&sm.b_empty[bs]);
                 }
-                if (i == 0) release_pending(0);  // the previous tile's stage slot
+                if (ii == 0) release_pending(0);  // the previous tile's stage slot
                 if (i == M - 1) stage_slot = vs;
                 // ring slots and phases of the next (tile, size) step
-                if (++vs == NV) { vs = 0; vph ^= 1; }
-                if (++bs == NB) { bs = 0; bph ^= 1; }
+                if (!STAGGER) {
+                    if (++vs == NV) { vs = 0; vph ^= 1; }
+                    if (++bs == NB) { bs = 0; bph ^= 1; }
+                }
             }
             if (KMD_DBG(1024)) {
                 pend = stage_slot;
