@@ -251,7 +251,13 @@ kmd_status kmd_band_step(void* comm, float* radiance, float* importance, const f
  * buffers make the copies asynchronous and overlappable).  The caller passes a
  * device workspace of at least kmd_host_workspace_bytes(N,H,W,cfg) bytes; the
  * work is pipelined in frame chunks across the copy engines.  The call returns
- * after enqueueing; synchronise `stream` before reading out_host.            */
+ * after enqueueing; synchronise `stream` before reading out_host.  Ordering:
+ * the kernels and device->host copies follow the work already queued on
+ * `stream`, and `stream` resumes after the last copy; the host->device copies
+ * (host inputs into the workspace) wait only until the workspace is free, so
+ * consecutive calls on one host thread stream their copies back to back.
+ * The workspace belongs to the library from the call until `stream` has
+ * passed it; the caller must not use it for other work in between.          */
 size_t kmd_host_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_config* cfg);
 kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
                                        const float* blend_host, float* out_host, int32_t N,

@@ -418,6 +418,9 @@ size_t host_frame_floats(int H, int W, int M, int rmax) {
 struct HostStreams {
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
     cudaEvent_t join = nullptr, done = nullptr;
+    // workspace carve of the last call (cross-call reuse of the band buffers)
+    const void* last_ws = nullptr;
+    int last_N = -1, last_H = -1, last_W = -1, last_M = -1, last_rmax = -1;
     cudaEvent_t in[2][HOST_MAX_BANDS] = {}, kern[2][HOST_MAX_BANDS] = {}, out[2][HOST_MAX_BANDS] = {};
     bool ok = false;
     int dev = -1;
@@ -511,10 +514,21 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     HostBand bb[HOST_MAX_BANDS];
     const int nb = host_bands(H, rmax, bb);
     cudaStream_t user = (cudaStream_t)stream;
-    // everything already queued on the caller's stream happens first
+    // the kernels and the D2H copies come after everything already queued on
+    // the caller's stream.  The H2D copies (host inputs into the workspace) wait
+    // only for the workspace: when this call carves it as the previous call on
+    // this thread did, band b's buffers wait for that call's band b D2H, so the
+    // copies of consecutive calls stream back to back; otherwise for the whole
+    // previous call
     if ((e = cudaEventRecord(hs->join, user)) != cudaSuccess) return cuda_fail(e, "event record");
-    for (cudaStream_t st : {hs->h2d, hs->comp, hs->d2h})
+    for (cudaStream_t st : {hs->comp, hs->d2h})
         if ((e = cudaStreamWaitEvent(st, hs->join, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
+    const bool same_carve = hs->last_ws == device_workspace && hs->last_N == N && hs->last_H == H &&
+                            hs->last_W == W && hs->last_M == M && hs->last_rmax == rmax;
+    if (!same_carve && (e = cudaStreamWaitEvent(hs->h2d, hs->done, 0)) != cudaSuccess)
+        return cuda_fail(e, "stream wait");
+    hs->last_ws = device_workspace; hs->last_N = N; hs->last_H = H; hs->last_W = W; hs->last_M = M;
+    hs->last_rmax = rmax;
     for (int n = 0; n < N; ++n) {
         const int set = n & 1;
         float* base = (float*)device_workspace + (size_t)(N > 1 ? set : 0) * frame_floats;
@@ -532,8 +546,10 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
             float* d_out = d_bl + (size_t)M * B.rows * W;
             cur = d_out + (size_t)3 * B.rows * W;
             cur = base + ((size_t)(cur - base) + 31 & ~(size_t)31);
-            // the buffers of this set were last used two frames ago: wait for that D2H
-            if (n >= 2 && (e = cudaStreamWaitEvent(hs->h2d, hs->out[set][b], 0)) != cudaSuccess)
+            // the buffers of this set were last used two frames ago (or by the
+            // previous call with the same carve): wait for that D2H
+            if ((n >= 2 || (n < 2 && same_carve)) &&
+                (e = cudaStreamWaitEvent(hs->h2d, hs->out[set][b], 0)) != cudaSuccess)
                 return cuda_fail(e, "stream wait");
             const int r0 = B.y0 - B.top;
             if ((e = copy_rows(d_rad, rh, W, H, 3, r0, buf_rows, true, hs->h2d)) != cudaSuccess ||

@@ -199,3 +199,18 @@ def test_unaligned_buffers(oracle_mod, cuda_device, N, H, W, sizes):
     torch.cuda.synchronize()
     assert kmd.last_kernel() == "v2-ws"
     assert_parity(out.cpu().numpy(), _oracle(oracle_mod, inp, sizes), what=f"unaligned {N}x{H}x{W}")
+
+
+def test_host_entry_point_back_to_back_calls(cuda_device):
+    # consecutive host calls reuse the workspace with their H2D copies streaming
+    # back to back (include/kmd.h): every call's output must still be its own
+    H, W = 130, 208
+    ws = torch.empty(kmd.host_workspace_bytes(1, H, W, PAPER), dtype=torch.uint8, device=cuda_device)
+    frames = [gen.make_inputs(1, H, W, 6, seed=300 + f) for f in range(4)]
+    outs = [torch.empty((1, 3, H, W)).pin_memory() for _ in frames]
+    hin = [(f.radiance.pin_memory(), f.importance.pin_memory(), f.blend.pin_memory()) for f in frames]
+    for (r, i, b), o in zip(hin, outs):
+        kmd.decode_filter_fuse_host(r, i, b, PAPER, o, ws)
+    torch.cuda.synchronize()
+    for f, o in zip(frames, outs):
+        assert np.array_equal(o.numpy(), _run(f, PAPER, cuda_device))
