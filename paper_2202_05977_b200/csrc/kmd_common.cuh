@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <utility>
 
 // Checked builds (-DKMD_CHECKS, scripts/build_variant.sh checked -DKMD_CHECKS):
 // device-side bounds / protocol assertions on every shared-memory index the
@@ -245,6 +246,39 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Programmatic dependent launch (KMD_PDL): a kernel launched with
+// launch_pdl may start (barrier setup, tensor-map prefetch) while the previous
+// kernel of the stream drains; pdl_wait() -- before the first global memory
+// access -- returns once that kernel has completed and its writes are
+// visible, so any producer / consumer order on the stream is kept.
+#ifndef KMD_PDL
+#define KMD_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if KMD_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if KMD_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <class... P, class... A>
+inline cudaError_t launch_pdl(void (*kern)(P...), int grid, int threads, size_t smem, cudaStream_t st,
+                              A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = KMD_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 constexpr float L2E = 1.44269502162933349609375f;        // log2(e) rounded to fp32
 // exp(x) = 2^t (1 + r) with t = fl(x log2 e) and r = x - t ln 2 (one FMA with
 // ln 2 rounded to fp32: the dropped t (ln 2 - fl(ln 2)) is below |t| 2^-28), to

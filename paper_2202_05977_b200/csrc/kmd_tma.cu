@@ -750,6 +750,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (TMEM_RAD) tmem_fence_before_sync();
     __syncthreads();
     if (TMEM_RAD) tmem_fence_after_sync();
+    // everything above touched only shared memory and the kernel parameters:
+    // with programmatic dependent launch it overlaps the previous kernel's tail
+    pdl_wait();
+    pdl_launch_dependents();
     const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 #ifdef KMD_INSTR
     unsigned long long instr[INSTR_TAGS] = {};
@@ -1343,8 +1347,8 @@ cudaError_t launch_bwd_h_tma(FusedParams p, float* ws, cudaStream_t stream) {
     if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return err;
     const int grid = (int)(n_tiles < sms ? n_tiles : sms);
-    kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, NTHREADS, smem, stream, p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y,
+                      (int)n_tiles);
 }
 
 bool tma_supported(const FusedParams& p) {
@@ -1393,8 +1397,8 @@ cudaError_t launch_fused_tma(FusedParams p, cudaStream_t stream) {
     auto launch = [&](auto kern) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
-        return cudaGetLastError();
+        return launch_pdl(kern, grid, NTHREADS, smem, stream, p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y,
+                          (int)n_tiles);
     };
     // specialisations: softmax fusion for M = 2..6 (the paper's M = 6, PAPER.md:324,
     // the multi-resolution levels' M = 2, the sweep-M configurations), M = 6 with
@@ -1460,8 +1464,8 @@ cudaError_t launch_fused_tma_mr(FusedParams p, cudaStream_t stream) {
     auto launch = [&](auto kern) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, NTHREADS, smem, stream>>>(p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y, (int)n_tiles);
-        return cudaGetLastError();
+        return launch_pdl(kern, grid, NTHREADS, smem, stream, p, m_rad, m_imp, m_blend, m_out, tiles_x, tiles_y,
+                          (int)n_tiles);
     };
     const bool softmax = p.blend != nullptr && p.blend_is_logits && p.M == 2;
     if (p.cmb_coarse) {
