@@ -169,6 +169,11 @@ constexpr int NV = KMD_NV;          // V ring depth (field -> fusion)
 #define KMD_L2PF 0
 #endif
 constexpr int L2PF = KMD_L2PF;
+// tiles whose boxes are prefetched into L2 at kernel start (before pdl_wait)
+#ifndef KMD_PF0
+#define KMD_PF0 1
+#endif
+constexpr int PF0 = KMD_PF0;
 constexpr unsigned TMEM_COLS = 256; // 4 columns (r, g, b, -) per box row: 4 x 39 <= 256
 // field warps; a field job is one (tile, size, 32-column half) walk, and the
 // jobs of consecutive tiles are dealt to the field warps round-robin in one
@@ -325,6 +330,15 @@ static_assert(sizeof(RadBuf) % 128 == 0 && sizeof(Slot) % 128 == 0 && sizeof(InS
 #ifdef KMD_INSTR
 constexpr int INSTR_TAGS = 16;
 __device__ unsigned long long g_instr[160 * 16 * INSTR_TAGS];
+// timeline (%globaltimer, ns): per CTA and warp [begin, end], and fusion
+// thread 0's tile-end times (first 16 tiles)
+__device__ unsigned long long g_tl[160 * 16 * 2];
+__device__ unsigned long long g_tt[160 * 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #define IWAIT(tag, call)                                         \
     do {                                                         \
         const long long t0_ = clock64();                         \
@@ -750,14 +764,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (TMEM_RAD) tmem_fence_before_sync();
     __syncthreads();
     if (TMEM_RAD) tmem_fence_after_sync();
+    const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     // everything above touched only shared memory and the kernel parameters:
-    // with programmatic dependent launch it overlaps the previous kernel's tail
+    // with programmatic dependent launch it overlaps the previous kernel's tail.
+    // So do L2 prefetches of the first PF0 tiles' boxes: a prefetch only moves
+    // lines into L2 (the point of coherence, which the previous kernel's writes
+    // reach too), so it may run before pdl_wait; the first tile's loads, all
+    // issued at once by every SM, then hit L2 instead of a 148-SM DRAM burst.
+    if (PF0 > 0 && warp == TMA_WARP && lane == 0) {
+        for (int tl = 0; tl < PF0 && tl < my_tiles; ++tl) {
+            const Tile pf = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            tma_prefetch_3d(&tm_rad, pf.x0 - XOFF, pf.y0 - RMAX - p.row_base, pf.n * 3);
+            for (int i = 0; i < M; ++i) {
+                tma_prefetch_3d(&tm_imp, pf.x0 - XOFF - xalign<SP::IN16>(pf.x0), pf.y0 - RMAX - p.row_base,
+                                pf.n * M + i);
+                if (has_blend)
+                    tma_prefetch_3d(&tm_blend, pf.x0 - xalign<SP::IN16>(pf.x0), pf.y0 - p.out_y0, pf.n * M + i);
+            }
+        }
+    }
     pdl_wait();
     pdl_launch_dependents();
-    const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 #ifdef KMD_INSTR
     unsigned long long instr[INSTR_TAGS] = {};
     const long long t_begin = clock64();
+    const unsigned long long g_begin = gtimer();
 #endif
 
     if (warp == TMA_WARP) {
@@ -973,7 +1004,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 // ---- backward pass A: h_i and G.R_i at this thread's pixels --------
                 // (whole frame: row_base = out_y0 = 0, buf_rows = out_rows = H)
                 const int gy = tc.y0 + ty;
-                const bool row_ok = active && gy < p.H;
                 const size_t plane = (size_t)p.H * p.W;
                 const int gyc = min(gy, p.H - 1);
                 const float* gp = p.grad + (size_t)tc.n * 3 * plane + (size_t)gyc * p.W;
@@ -1254,6 +1284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             pend = stage_slot;  // released after the next tile's first size (or never: kernel end)
 #ifdef KMD_INSTR
             instr[13] += (unsigned long long)(clock64() - t_epi);
+            if (c == 0 && tl < 16 && blockIdx.x < 160) g_tt[blockIdx.x * 16 + tl] = gtimer();
 #endif
         }
         if (c == 0) bulk_wait0();
@@ -1269,6 +1300,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 #ifdef KMD_INSTR
     instr[15] = (unsigned long long)(clock64() - t_begin);
+    if (lane == 0 && blockIdx.x < 160) {
+        g_tl[(blockIdx.x * 16 + warp) * 2] = g_begin;
+        g_tl[(blockIdx.x * 16 + warp) * 2 + 1] = gtimer();
+    }
     if (lane == 0 && blockIdx.x < 160)
         for (int t = 0; t < INSTR_TAGS; ++t) g_instr[(blockIdx.x * 16 + warp) * INSTR_TAGS + t] = instr[t];
 #endif
@@ -1313,6 +1348,11 @@ bool make_map(CUtensorMap* m, const float* base, int W, int rows, long long plan
 #ifdef KMD_INSTR
 extern "C" int kmd_debug_read_instr(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, tma::g_instr, sizeof(unsigned long long) * n);
+}
+extern "C" int kmd_debug_read_timeline(unsigned long long* tl, unsigned long long* tt) {
+    cudaError_t e = cudaMemcpyFromSymbol(tl, tma::g_tl, sizeof(tma::g_tl));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(tt, tma::g_tt, sizeof(tma::g_tt));
+    return (int)e;
 }
 #endif
 
