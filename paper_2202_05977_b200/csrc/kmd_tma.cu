@@ -369,6 +369,14 @@ __device__ __forceinline__ Tile tile_of(const FusedParams& p, int t, int tiles_x
     return c;
 }
 
+// The linear tile index of this CTA's tl-th tile: waves of gridDim.x tiles in
+// row-major order, so CTA b keeps tile column b % tiles_x when gridDim.x is a
+// multiple of tiles_x (1080p).  Measured and not kept: rotating the CTAs over
+// the wave's tile rows from wave to wave (57.1 vs 54.8 us per 1080p frame).
+__device__ __forceinline__ int tile_index(int tl, int /*tiles_x*/, int /*n_tiles*/) {
+    return blockIdx.x + tl * (int)gridDim.x;
+}
+
 // Border rows (clamp-to-edge, reading R1): read through a clamped row index by
 // a second, border-tile instantiation of the field loop (KMD_CLAMP_VARIANT 1,
 // default: no generic writes to the TMA boxes), or replicated into the boxes
@@ -773,7 +781,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // issued at once by every SM, then hit L2 instead of a 148-SM DRAM burst.
     if (PF0 > 0 && warp == TMA_WARP && lane == 0) {
         for (int tl = 0; tl < PF0 && tl < my_tiles; ++tl) {
-            const Tile pf = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            const Tile pf = tile_of(p, tile_index(tl, tiles_x, n_tiles), tiles_x, tiles_y);
             tma_prefetch_3d(&tm_rad, pf.x0 - XOFF, pf.y0 - RMAX - p.row_base, pf.n * 3);
             for (int i = 0; i < M; ++i) {
                 tma_prefetch_3d(&tm_imp, pf.x0 - XOFF - xalign<SP::IN16>(pf.x0), pf.y0 - RMAX - p.row_base,
@@ -805,12 +813,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // Deadlock-free: each wait is on a slot released by a step whose
             // inputs were issued earlier.
             for (int tl = 0; tl < my_tiles; ++tl) {
-                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                const Tile tc = tile_of(p, tile_index(tl, tiles_x, n_tiles), tiles_x, tiles_y);
                 const int rb = tl % NRAD;
                 if (L2PF > 0 && tl + L2PF < my_tiles) {
                     // HBM -> L2 prefetch of a later tile's boxes (no shared memory,
                     // no barrier): its TMA loads then hit L2
-                    const Tile pf = tile_of(p, blockIdx.x + (tl + L2PF) * gridDim.x, tiles_x, tiles_y);
+                    const Tile pf = tile_of(p, tile_index(tl + L2PF, tiles_x, n_tiles), tiles_x, tiles_y);
                     tma_prefetch_3d(&tm_rad, pf.x0 - XOFF, pf.y0 - RMAX - p.row_base, pf.n * 3);
                     for (int i = 0; i < M; ++i) {
                         tma_prefetch_3d(&tm_imp, pf.x0 - XOFF - xalign<SP::IN16>(pf.x0), pf.y0 - RMAX - p.row_base,
@@ -854,7 +862,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             constexpr unsigned ESZ = SP::IN16 ? 2 : 4;
             constexpr unsigned B_BYTES = TH * InElem<SP::IN16>::BBW * ESZ;
             for (int tl = 0; tl < my_tiles; ++tl) {
-                const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+                const Tile tc = tile_of(p, tile_index(tl, tiles_x, n_tiles), tiles_x, tiles_y);
                 for (int i = 0; i < M; ++i) {
                     const int seq = tl * M + i, sb = seq % NB;
                     IWAIT(8, mbar_wait(&sm.b_empty[sb], ((seq / NB) & 1) ^ 1));
@@ -880,7 +888,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const unsigned tm = TMEM_RAD ? sm.tmem_base + ((unsigned)(32 * (warp & 3)) << 16) : 0u;
         int g = fw;
         for (int tl = 0; tl < my_tiles; ++tl) {
-            const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            const Tile tc = tile_of(p, tile_index(tl, tiles_x, n_tiles), tiles_x, tiles_y);
             const int rb = tl % NRAD;
             IWAIT(2, mbar_wait(&sm.rad_full[rb], (tl / NRAD) & 1));
             if constexpr (TMEM_RAD) {
@@ -999,7 +1007,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
         };
         for (int tl = 0; tl < my_tiles; ++tl) {
-            const Tile tc = tile_of(p, blockIdx.x + tl * gridDim.x, tiles_x, tiles_y);
+            const Tile tc = tile_of(p, tile_index(tl, tiles_x, n_tiles), tiles_x, tiles_y);
             if constexpr (SP::MODE == FUSE_BWD_H) {
                 // ---- backward pass A: h_i and G.R_i at this thread's pixels --------
                 // (whole frame: row_base = out_y0 = 0, buf_rows = out_rows = H)
