@@ -17,7 +17,8 @@ def _dev(t, d):
     return None if t is None else t.to(d)
 
 
-@pytest.mark.parametrize("N,H,W", [(1, 96, 160), (2, 72, 104), (1, 36, 44), (1, 540, 960)])
+@pytest.mark.parametrize("N,H,W", [(1, 96, 160), (2, 72, 104), (1, 36, 44), (1, 540, 960), (2, 112, 208),
+                                   (3, 56, 112)])
 def test_mr_matches_oracle(oracle_mod, cuda_device, N, H, W):
     sizes = [list(s) for s in gen.MR_SIZES]
     mi = gen.make_mr_inputs(N, H, W)
