@@ -343,7 +343,7 @@ def run_kmd(args, rank, world, local):
 
     # ---- e2e: through the C ABI with pinned HOST buffers ---------------------
     e2e = None
-    if args.e2e_steps > 0 and not args.bf16:  # the host entry point is fp32-only
+    if args.e2e_steps > 0:  # bf16 importance / logits: kmd_decode_filter_fuse_host_bf16
         hr = inp.radiance[:1].cpu().pin_memory()
         hi = inp.importance[:1].cpu().pin_memory()
         hb = None if inp.blend is None else inp.blend[:1].cpu().pin_memory()
@@ -360,11 +360,12 @@ def run_kmd(args, rank, world, local):
         b.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = max_over_ranks(a.elapsed_time(b), world)
-        h2d = (hr.numel() + hi.numel() + (0 if hb is None else hb.numel())) * 4
+        h2d = sum(t.numel() * t.element_size() for t in (hr, hi, hb) if t is not None)
         e2e = {"value": px_per_step * args.e2e_steps / (e2e_ms / 1e3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": ho.numel() * 4,
                "ms_per_step": e2e_ms / args.e2e_steps,
-               "path": "kmd_decode_filter_fuse_host (pinned host -> HBM -> kernel -> host)"}
+               "path": ("kmd_decode_filter_fuse_host_bf16" if args.bf16 else "kmd_decode_filter_fuse_host") +
+                       " (pinned host -> HBM -> kernel -> host)"}
 
     # ---- CPU oracle baseline + sampled parity (rank 0, N=1 only) -------------
     cpu = None

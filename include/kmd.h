@@ -264,6 +264,17 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
                                        int32_t H, int32_t W, const kmd_config* cfg,
                                        void* device_workspace, size_t workspace_bytes,
                                        kmd_stream_t stream);
+/* The same with bf16 importance maps and fusion logits in host memory (the
+ * network's output at 2 B per value: 75 instead of 124 MB of host->device
+ * copies per 1080p M = 6 frame); the kernel is kmd_decode_filter_fuse_bf16's
+ * (bf16 widened exactly to fp32, R24), run per band.  Needs W % 8
+ * == 0 and sizes <= 13 (else KMD_ERR_ALIGN / KMD_ERR_CONFIG); the workspace
+ * size is kmd_host_workspace_bytes(...) as above.                           */
+kmd_status kmd_decode_filter_fuse_host_bf16(const float* radiance_host, const uint16_t* importance_host,
+                                            const uint16_t* blend_host, float* out_host, int32_t N,
+                                            int32_t H, int32_t W, const kmd_config* cfg,
+                                            void* device_workspace, size_t workspace_bytes,
+                                            kmd_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT row 2: the multi-resolution "Ours MR" reconstruction (PAPER.md:313-318

@@ -262,7 +262,7 @@ namespace {
 // kmd_decode_filter_fuse_band).  Returns KMD_OK with *skip = true when N == 0.
 kmd_status band_params(const float* radiance, const float* importance, const float* blend, float* out, int32_t N,
                        int32_t band_rows, int32_t W, int32_t halo_top, int32_t halo_bot, int32_t y0,
-                       int32_t H_global, const kmd_config* cfg, kmd::FusedParams* p, bool* skip) {
+                       int32_t H_global, const kmd_config* cfg, kmd::FusedParams* p, bool* skip, int in16 = 0) {
     *skip = false;
     if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
     if (!cfg) return fail(KMD_ERR_NULL, "cfg is NULL");
@@ -291,12 +291,13 @@ kmd_status band_params(const float* radiance, const float* importance, const flo
     if (cfg->num_sizes > 1 && !blend) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
     const int buf_rows = halo_top + band_rows + halo_bot;
     const size_t bplane = (size_t)buf_rows * W * sizeof(float), oplane = (size_t)band_rows * W * sizeof(float);
-    const size_t M = (size_t)cfg->num_sizes;
+    const size_t M = (size_t)cfg->num_sizes, esz = in16 ? 2 : 4;
     if (overlaps(out, 3 * N * oplane, radiance, 3 * N * bplane) ||
-        overlaps(out, 3 * N * oplane, importance, M * N * bplane) ||
-        (M > 1 && overlaps(out, 3 * N * oplane, blend, M * N * oplane)))
+        overlaps(out, 3 * N * oplane, importance, M * N * bplane / 4 * esz) ||
+        (M > 1 && overlaps(out, 3 * N * oplane, blend, M * N * oplane / 4 * esz)))
         return fail(KMD_ERR_ALIAS, "out overlaps an input");
     kmd::FusedParams q{};
+    q.in16 = in16;
     q.rad = radiance; q.imp = importance; q.blend = blend; q.out = out;
     q.N = N; q.W = W; q.H = H_global;
     q.row_base = y0 - halo_top; q.buf_rows = buf_rows; q.out_y0 = y0; q.out_rows = band_rows;
@@ -420,7 +421,7 @@ struct HostStreams {
     cudaEvent_t join = nullptr, done = nullptr;
     // workspace carve of the last call (cross-call reuse of the band buffers)
     const void* last_ws = nullptr;
-    int last_N = -1, last_H = -1, last_W = -1, last_M = -1, last_rmax = -1;
+    int last_N = -1, last_H = -1, last_W = -1, last_M = -1, last_rmax = -1, last_in16 = -1;
     cudaEvent_t in[2][HOST_MAX_BANDS] = {}, kern[2][HOST_MAX_BANDS] = {}, out[2][HOST_MAX_BANDS] = {};
     bool ok = false;
     int dev = -1;
@@ -457,10 +458,10 @@ cudaError_t host_streams(HostStreams** hs) {
 // rows [r0, r0+nr) of `planes` planes of an [planes][H][W] host tensor <-> a
 // dense [planes][nr][W] device buffer, one 3-D copy
 cudaError_t copy_rows(void* dev, const void* host, int W, int H, int planes, int r0, int nr, bool to_dev,
-                      cudaStream_t st) {
+                      cudaStream_t st, size_t esz = sizeof(float)) {
     cudaMemcpy3DParms c = {};
-    const size_t pitch = (size_t)W * sizeof(float);
-    cudaPitchedPtr hp = make_cudaPitchedPtr((void*)((const float*)host + (size_t)r0 * W), pitch, W, H);
+    const size_t pitch = (size_t)W * esz;
+    cudaPitchedPtr hp = make_cudaPitchedPtr((void*)((const char*)host + (size_t)r0 * pitch), pitch, W, H);
     cudaPitchedPtr dp = make_cudaPitchedPtr(dev, pitch, W, nr);
     if (to_dev) {
         c.srcPtr = hp;
@@ -485,11 +486,13 @@ size_t kmd_host_workspace_bytes(int32_t N, int32_t H, int32_t W, const kmd_confi
     return frame * (N > 1 ? 2 : 1);  // two frames in flight when N > 1
 }
 
-kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
-                                       const float* blend_host, float* out_host, int32_t N,
-                                       int32_t H, int32_t W, const kmd_config* cfg,
-                                       void* device_workspace, size_t workspace_bytes,
-                                       kmd_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// the host entry points (fp32 or bf16 importance / logits in host memory)
+kmd_status host_entry(const float* radiance_host, const void* importance_host, const void* blend_host,
+                      float* out_host, int32_t N, int32_t H, int32_t W, const kmd_config* cfg,
+                      void* device_workspace, size_t workspace_bytes, kmd_stream_t stream, int in16) {
     g_err[0] = 0;
     if (N < 0) return fail(KMD_ERR_DIM, "N=%d < 0", N);
     if (N > 0 && (H < 1 || W < 1)) return fail(KMD_ERR_DIM, "H=%d, W=%d must be >= 1", H, W);
@@ -502,6 +505,14 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     if (!radiance_host || !importance_host || !out_host || !device_workspace)
         return fail(KMD_ERR_NULL, "a host buffer or the workspace is NULL");
     if (cfg->num_sizes > 1 && !blend_host) return fail(KMD_ERR_NULL, "blend is NULL with M=%d > 1", cfg->num_sizes);
+    if (in16) {
+        if (W % 8 != 0) return fail(KMD_ERR_ALIGN, "bf16 path needs W %% 8 == 0 (W=%d)", W);
+        for (int k = 0; k < cfg->num_sizes; ++k)
+            if ((cfg->sizes[k] - 1) / 2 > 6)
+                return fail(KMD_ERR_CONFIG, "bf16 path supports sizes <= 13 (sizes[%d]=%d)", k, cfg->sizes[k]);
+        if ((uintptr_t)device_workspace & 15) return fail(KMD_ERR_ALIGN, "bf16 path needs a 16-byte aligned workspace");
+    }
+    const size_t esz = in16 ? 2 : 4;
     const size_t need = kmd_host_workspace_bytes(N, H, W, cfg);
     if (workspace_bytes < need)
         return fail(KMD_ERR_DIM, "workspace %zu bytes < required %zu", workspace_bytes, need);
@@ -524,17 +535,18 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     for (cudaStream_t st : {hs->comp, hs->d2h})
         if ((e = cudaStreamWaitEvent(st, hs->join, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     const bool same_carve = hs->last_ws == device_workspace && hs->last_N == N && hs->last_H == H &&
-                            hs->last_W == W && hs->last_M == M && hs->last_rmax == rmax;
+                            hs->last_W == W && hs->last_M == M && hs->last_rmax == rmax && hs->last_in16 == in16;
     if (!same_carve && (e = cudaStreamWaitEvent(hs->h2d, hs->done, 0)) != cudaSuccess)
         return cuda_fail(e, "stream wait");
     hs->last_ws = device_workspace; hs->last_N = N; hs->last_H = H; hs->last_W = W; hs->last_M = M;
     hs->last_rmax = rmax;
+    hs->last_in16 = in16;
     for (int n = 0; n < N; ++n) {
         const int set = n & 1;
         float* base = (float*)device_workspace + (size_t)(N > 1 ? set : 0) * frame_floats;
         const float* rh = radiance_host + (size_t)n * 3 * plane;
-        const float* ih = importance_host + (size_t)n * M * plane;
-        const float* bh = M > 1 ? blend_host + (size_t)n * M * plane : nullptr;
+        const char* ih = (const char*)importance_host + (size_t)n * M * plane * esz;
+        const char* bh = M > 1 ? (const char*)blend_host + (size_t)n * M * plane * esz : nullptr;
         float* oh = out_host + (size_t)n * 3 * plane;
         float* cur = base;
         for (int b = 0; b < nb; ++b) {
@@ -553,13 +565,16 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
                 return cuda_fail(e, "stream wait");
             const int r0 = B.y0 - B.top;
             if ((e = copy_rows(d_rad, rh, W, H, 3, r0, buf_rows, true, hs->h2d)) != cudaSuccess ||
-                (e = copy_rows(d_imp, ih, W, H, M, r0, buf_rows, true, hs->h2d)) != cudaSuccess ||
-                (bh && (e = copy_rows(d_bl, bh, W, H, M, B.y0, B.rows, true, hs->h2d)) != cudaSuccess))
+                (e = copy_rows(d_imp, ih, W, H, M, r0, buf_rows, true, hs->h2d, esz)) != cudaSuccess ||
+                (bh && (e = copy_rows(d_bl, bh, W, H, M, B.y0, B.rows, true, hs->h2d, esz)) != cudaSuccess))
                 return cuda_fail(e, "H2D band copy");
             if ((e = cudaEventRecord(hs->in[set][b], hs->h2d)) != cudaSuccess) return cuda_fail(e, "event record");
             if ((e = cudaStreamWaitEvent(hs->comp, hs->in[set][b], 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
-            kmd_status s = kmd_decode_filter_fuse_band(d_rad, d_imp, bh ? d_bl : nullptr, d_out, 1, B.rows, W,
-                                                       B.top, B.bot, B.y0, H, cfg, hs->comp);
+            kmd::FusedParams bp{};
+            bool skip = false;
+            kmd_status s = band_params(d_rad, d_imp, bh ? d_bl : nullptr, d_out, 1, B.rows, W, B.top, B.bot, B.y0, H,
+                                       cfg, &bp, &skip, in16);
+            if (!s && !skip) s = run_fused(bp, cfg, hs->comp);
             if (s) return s;
             if ((e = cudaEventRecord(hs->kern[set][b], hs->comp)) != cudaSuccess) return cuda_fail(e, "event record");
             if ((e = cudaStreamWaitEvent(hs->d2h, hs->kern[set][b], 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
@@ -572,6 +587,27 @@ kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* 
     if ((e = cudaEventRecord(hs->done, hs->d2h)) != cudaSuccess) return cuda_fail(e, "event record");
     if ((e = cudaStreamWaitEvent(user, hs->done, 0)) != cudaSuccess) return cuda_fail(e, "stream wait");
     return KMD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+kmd_status kmd_decode_filter_fuse_host(const float* radiance_host, const float* importance_host,
+                                       const float* blend_host, float* out_host, int32_t N,
+                                       int32_t H, int32_t W, const kmd_config* cfg,
+                                       void* device_workspace, size_t workspace_bytes,
+                                       kmd_stream_t stream) {
+    return host_entry(radiance_host, importance_host, blend_host, out_host, N, H, W, cfg, device_workspace,
+                      workspace_bytes, stream, 0);
+}
+
+kmd_status kmd_decode_filter_fuse_host_bf16(const float* radiance_host, const uint16_t* importance_host,
+                                            const uint16_t* blend_host, float* out_host, int32_t N,
+                                            int32_t H, int32_t W, const kmd_config* cfg,
+                                            void* device_workspace, size_t workspace_bytes,
+                                            kmd_stream_t stream) {
+    return host_entry(radiance_host, importance_host, blend_host, out_host, N, H, W, cfg, device_workspace,
+                      workspace_bytes, stream, 1);
 }
 
 // ---------------------------------------------------------------------------

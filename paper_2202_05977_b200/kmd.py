@@ -77,7 +77,7 @@ EXPORTS = ("kmd_decode_filter_fuse", "kmd_decode_filter_fuse_bf16", "kmd_decode_
            "kmd_decode_filter_fuse_band", "kmd_decode_filter_fuse_band_part", "kmd_nccl_unique_id",
            "kmd_comm_init", "kmd_comm_destroy", "kmd_halo_exchange", "kmd_band_step",
            "kmd_host_workspace_bytes",
-           "kmd_decode_filter_fuse_host", "kmd_algorithmic_bytes", "kmd_launches_per_call",
+           "kmd_decode_filter_fuse_host", "kmd_decode_filter_fuse_host_bf16", "kmd_algorithmic_bytes", "kmd_launches_per_call",
            "kmd_status_string", "kmd_last_error", "kmd_version", "kmd_last_kernel")
 
 
@@ -122,6 +122,7 @@ def lib(build_if_missing: bool = True):
     L.kmd_host_workspace_bytes.argtypes = [i32, i32, i32, C]
     L.kmd_host_workspace_bytes.restype = ctypes.c_size_t
     L.kmd_decode_filter_fuse_host.argtypes = [P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
+    L.kmd_decode_filter_fuse_host_bf16.argtypes = [P, P, P, P, i32, i32, i32, C, P, ctypes.c_size_t, P]
     L.kmd_algorithmic_bytes.argtypes = [i32, i32, i32, C, i32]
     L.kmd_algorithmic_bytes.restype = ctypes.c_int64
     L.kmd_launches_per_call.argtypes = []
@@ -423,23 +424,27 @@ def decode_filter_fuse_host(radiance: torch.Tensor, importance: torch.Tensor,
     """End-to-end from host (ideally pinned) CPU tensors: H2D copies, fused
     kernel and D2H copy, all enqueued by libkmd on ``stream``.  ``workspace`` is
     a CUDA uint8 tensor of >= host_workspace_bytes(...) bytes.  Returns ``out``
-    (caller synchronises ``stream`` before reading it)."""
+    (caller synchronises ``stream`` before reading it).  importance / blend in
+    bfloat16 (both) take kmd_decode_filter_fuse_host_bf16."""
     N, _, H, W = radiance.shape
     M = len(sizes)
-    for name, t, shape in (("radiance", radiance, (N, 3, H, W)),
-                           ("importance", importance, (N, M, H, W)),
-                           ("out", out, (N, 3, H, W))):
-        if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() \
-                or tuple(t.shape) != shape:
-            raise ValueError(f"{name} must be a contiguous float32 CPU tensor of shape {shape}")
-    if blend is not None and (blend.device.type != "cpu" or tuple(blend.shape) != (N, M, H, W)):
-        raise ValueError("blend must be a contiguous float32 CPU tensor [N,M,H,W]")
+    in16 = importance.dtype == torch.bfloat16
+    idt = torch.bfloat16 if in16 else torch.float32
+    for name, t, shape, dt in (("radiance", radiance, (N, 3, H, W), torch.float32),
+                               ("importance", importance, (N, M, H, W), idt),
+                               ("out", out, (N, 3, H, W), torch.float32)):
+        if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous() or tuple(t.shape) != shape:
+            raise ValueError(f"{name} must be a contiguous {dt} CPU tensor of shape {shape}")
+    if blend is not None and (blend.device.type != "cpu" or tuple(blend.shape) != (N, M, H, W)
+                              or blend.dtype != idt or not blend.is_contiguous()):
+        raise ValueError(f"blend must be a contiguous {idt} CPU tensor [N,M,H,W] (importance's dtype)")
     if workspace.device.type != "cuda":
         raise ValueError("workspace must be a CUDA tensor")
     cfg = make_config(sizes, blend_is_logits)
     if stream is None:
         stream = torch.cuda.current_stream(workspace.device)
-    _check(lib().kmd_decode_filter_fuse_host(
+    entry = lib().kmd_decode_filter_fuse_host_bf16 if in16 else lib().kmd_decode_filter_fuse_host
+    _check(entry(
         radiance.data_ptr(), importance.data_ptr(),
         None if blend is None else blend.data_ptr(), out.data_ptr(), N, H, W,
         ctypes.byref(cfg), workspace.data_ptr(), workspace.numel() * workspace.element_size(),

@@ -108,3 +108,28 @@ def test_bf16_errors(cuda_device):
     with pytest.raises(ValueError):
         kmd.decode_filter_fuse(inp.radiance, i16, b16, [3, 5], albedo=torch.ones_like(inp.radiance))
     assert kmd.decode_filter_fuse(inp.radiance[:0], i16[:0], b16[:0], [3, 5]).shape[0] == 0
+
+
+@pytest.mark.parametrize("N,H,W,sizes", [(2, 120, 200, PAPER), (1, 61, 104, [3, 5, 7]), (1, 48, 64, [5])])
+def test_bf16_host_entry_matches_device_path_bitwise(oracle_mod, cuda_device, N, H, W, sizes):
+    # kmd_decode_filter_fuse_host_bf16: bf16 importance / logits from pinned
+    # host memory, per-band kernels on the same global tile grid -> the device
+    # bf16 path bit for bit, and the oracle on the widened values
+    inp = gen.make_inputs(N, H, W, len(sizes), seed=4100 + W)
+    i16, b16, _, _ = _bf16(inp)
+    dev = _run16(inp, sizes, cuda_device).cpu().numpy()
+    out = torch.empty((N, 3, H, W)).pin_memory()
+    ws = torch.empty(kmd.host_workspace_bytes(N, H, W, sizes), dtype=torch.uint8, device=cuda_device)
+    kmd.decode_filter_fuse_host(inp.radiance.pin_memory(), i16.pin_memory(),
+                                None if b16 is None else b16.pin_memory(), sizes, out, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.numpy(), dev)
+    assert_parity(out.numpy(), _oracle(oracle_mod, inp, sizes), what=f"bf16 host {N}x{H}x{W}")
+
+
+def test_bf16_host_entry_rejects_unaligned_width(cuda_device):
+    inp = gen.make_inputs(1, 32, 60, 2)
+    i16, b16, _, _ = _bf16(inp)
+    ws = torch.empty(kmd.host_workspace_bytes(1, 32, 60, [3, 5]), dtype=torch.uint8, device=cuda_device)
+    with pytest.raises(kmd.KmdError, match="ALIGN"):
+        kmd.decode_filter_fuse_host(inp.radiance, i16, b16, [3, 5], torch.empty((1, 3, 32, 60)), ws)
