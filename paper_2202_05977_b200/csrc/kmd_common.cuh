@@ -265,11 +265,11 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 #endif
 }
 template <class... P, class... A>
-inline cudaError_t launch_pdl(void (*kern)(P...), int grid, int threads, size_t smem, cudaStream_t st,
+inline cudaError_t launch_pdl(void (*kern)(P...), dim3 grid, dim3 threads, size_t smem, cudaStream_t st,
                               A&&... args) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads);
+    cfg.gridDim = grid;
+    cfg.blockDim = threads;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
