@@ -214,3 +214,26 @@ def test_host_entry_point_back_to_back_calls(cuda_device):
     torch.cuda.synchronize()
     for f, o in zip(frames, outs):
         assert np.array_equal(o.numpy(), _run(f, PAPER, cuda_device))
+
+
+def test_dependent_launches_read_the_previous_output(cuda_device):
+    # The TMA kernel is launched with programmatic dependent launch and may
+    # start while the previous kernel on the stream drains: every global access
+    # waits on griddepcontrol.wait.  Chain three launches, each reading the
+    # previous one's output as its radiance, with nothing in between, and
+    # compare with the same chain synchronised after every launch.
+    H, W = 96, 160
+    frames = [gen.make_inputs(1, H, W, 6, seed=700 + k) for k in range(3)]
+    r0 = frames[0].radiance.to(cuda_device)
+    ins = [(f.importance.to(cuda_device), f.blend.to(cuda_device)) for f in frames]
+    x = r0
+    for i, b in ins:  # back to back
+        x = kmd.decode_filter_fuse(x, i, b, PAPER)
+    chained = x.cpu().numpy()
+    y = r0
+    for i, b in ins:
+        torch.cuda.synchronize()
+        y = kmd.decode_filter_fuse(y.clone(), i, b, PAPER)
+        torch.cuda.synchronize()
+    assert kmd.last_kernel() == "v3-tma-M6"
+    assert np.array_equal(chained, y.cpu().numpy())
