@@ -607,7 +607,14 @@ def backward_launches_per_call(M: int, path: Optional[str] = None, blend_is_logi
 
 class DecodeFilterFuse(torch.autograd.Function):
     """Differentiable kmd_decode_filter_fuse (w.r.t. importance and blend):
-    forward and backward both run in libkmd."""
+    forward and backward both run in libkmd.  The backward evaluates exp(I)
+    unshifted (include/kmd.h: importance in (-80, 80)); with ``check_range``
+    (default) an importance map outside that range raises ValueError instead
+    of returning inf / NaN gradients (one device reduction and one host sync
+    per backward call)."""
+
+    check_range = True
+    IMPORTANCE_LIMIT = 80.0
 
     @staticmethod
     def forward(ctx, radiance, importance, blend, sizes, blend_is_logits=True):
@@ -619,6 +626,13 @@ class DecodeFilterFuse(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad_out):
         radiance, importance, blend = ctx.saved_tensors
+        if DecodeFilterFuse.check_range and importance.numel() > 0:
+            m = float(importance.abs().amax())
+            if not m < DecodeFilterFuse.IMPORTANCE_LIMIT:
+                raise ValueError(f"DecodeFilterFuse.backward: max |importance| = {m:g} is outside the "
+                                 f"backward's range (-{DecodeFilterFuse.IMPORTANCE_LIMIT:g}, "
+                                 f"{DecodeFilterFuse.IMPORTANCE_LIMIT:g}) (include/kmd.h); "
+                                 "shift the importance maps (the decoder is shift-invariant, PAPER.md:154)")
         gI, gB = decode_filter_fuse_backward(radiance, importance, blend, grad_out.contiguous(),
                                              ctx.sizes, ctx.logits)
         return None, gI, gB, None, None

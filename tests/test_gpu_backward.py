@@ -105,6 +105,19 @@ def test_autograd_function(oracle_mod, cuda_device):
     _normwise(B.grad.cpu().numpy(), rB, "autograd grad_blend")
 
 
+def test_autograd_rejects_importance_outside_backward_range(cuda_device):
+    # the forward takes any finite importance (exact fallback); the backward's
+    # unshifted exp(I) needs |I| < 80, which the autograd wrapper checks
+    sizes = [3, 5]
+    inp = gen.make_inputs(1, 32, 48, 2, seed=29)
+    I = (inp.importance + 85.0).to(cuda_device).requires_grad_(True)
+    B = inp.blend.to(cuda_device).requires_grad_(True)
+    out = kmd.DecodeFilterFuse.apply(inp.radiance.to(cuda_device), I, B, sizes)
+    assert torch.isfinite(out).all()
+    with pytest.raises(ValueError, match="backward's range"):
+        out.sum().backward()
+
+
 def test_backward_empty_and_errors(cuda_device):
     z = torch.empty((0, 3, 8, 8), device=cuda_device)
     zi = torch.empty((0, 2, 8, 8), device=cuda_device)
