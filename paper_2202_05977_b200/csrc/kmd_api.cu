@@ -380,7 +380,13 @@ kmd_status kmd_decode_filter_fuse_band_part(const float* radiance, const float* 
 // joined at the start and the end, so the call behaves as stream-ordered work.
 namespace {
 
-constexpr int HOST_MAX_BANDS = 4;
+#ifndef KMD_HOST_BANDS
+#define KMD_HOST_BANDS 2
+#endif
+#ifndef KMD_HOST_LASTW
+#define KMD_HOST_LASTW 3  // weight of the last band (the others: 5)
+#endif
+constexpr int HOST_MAX_BANDS = KMD_HOST_BANDS;
 
 struct HostBand {
     int y0, rows, top, bot;  // owned rows [y0, y0+rows), halo rows above/below
@@ -388,10 +394,14 @@ struct HostBand {
 
 int host_bands(int H, int rmax, HostBand* out) {
     int nb = HOST_MAX_BANDS;
-    while (nb > 1 && (int64_t)2 * H / (5 * (nb - 1) + 2) < 2 * rmax + 8) --nb;
-    // the last band is 0.4 of the others: the call ends with that band's kernel
-    // and D2H, which nothing overlaps (the H2D stream is the critical path)
-    const int64_t wsum = 5 * (nb - 1) + 2;
+    while (nb > 1 && (int64_t)KMD_HOST_LASTW * H / (5 * (nb - 1) + KMD_HOST_LASTW) < 2 * rmax + 8) --nb;
+    // Two bands, the last 3/5 of the first (KMD_HOST_BANDS, KMD_HOST_LASTW):
+    // the call ends with the last band's kernel and D2H, which nothing
+    // overlaps, while more, smaller copies lose PCIe throughput.  Measured
+    // (1080p M = 6, consecutive calls): 4 bands 832 / 1292 Mpix/s (fp32 /
+    // bf16 inputs), 3 bands 848 / 1328, 2 bands 5:2 871 / 1354, 2 bands 5:3
+    // 874 / 1414, 2 bands 5:5 850 / 1369, 1 band 742 / 1094.
+    const int64_t wsum = 5 * (nb - 1) + KMD_HOST_LASTW;
     auto edge = [&](int b) { return (int)(b == nb ? H : (int64_t)5 * b * H / wsum); };
     for (int b = 0; b < nb; ++b) {
         const int y0 = edge(b), y1 = edge(b + 1);
