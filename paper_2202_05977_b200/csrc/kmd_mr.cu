@@ -46,8 +46,12 @@ __global__ void __launch_bounds__(256) down2_kernel(const float* __restrict__ in
 // 2x2 mean of the level below in the same fp32 order as down2_kernel (so the
 // bits equal two down2 passes).  H0, W0 divisible by 4.
 template <bool VEC>
-__global__ void __launch_bounds__(256) down4_kernel(const float* __restrict__ in, float* __restrict__ out1,
+__global__ void __launch_bounds__(256, 8) down4_kernel(const float* __restrict__ in, float* __restrict__ out1,
                                                     float* __restrict__ out2, int planes, int H2, int W2) {
+    // one resident wave (launch_down4): triggering the dependent launch now
+    // cannot starve this grid, and the level kernel's setup and first-tile
+    // prefetch overlap the rest of it
+    pdl_launch_dependents();
     const int W0 = 4 * W2, W1 = 2 * W2;
     const long long total = (long long)planes * H2 * W2;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -139,10 +143,15 @@ cudaError_t launch_down2(const float* in, float* out, long long planes, int Ho, 
 cudaError_t launch_down4(const float* in, float* out1, float* out2, int planes, int H2, int W2, cudaStream_t st) {
     const long long n = (long long)planes * H2 * W2;
     if (n == 0) return cudaSuccess;
+    // at most one wave of 8 resident 256-thread CTAs per SM (grid-stride)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = grid_for(n) < sms * 8 ? grid_for(n) : sms * 8;
     if (((uintptr_t)in & 15) == 0)
-        down4_kernel<true><<<grid_for(n), 256, 0, st>>>(in, out1, out2, planes, H2, W2);
+        down4_kernel<true><<<g, 256, 0, st>>>(in, out1, out2, planes, H2, W2);
     else
-        down4_kernel<false><<<grid_for(n), 256, 0, st>>>(in, out1, out2, planes, H2, W2);
+        down4_kernel<false><<<g, 256, 0, st>>>(in, out1, out2, planes, H2, W2);
     return cudaGetLastError();
 }
 
