@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--sizes", type=str, default=",".join(map(str, PAPER_SIZES)))
     ap.add_argument("--rotate", type=int, default=4, help="distinct resident frames per rank")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--batch", type=int, default=256,
                     help="--mode batch: frames in the whole batch, sharded over the ranks (BASELINE.json configs[4])")
     ap.add_argument("--albedo", action="store_true",
