@@ -61,10 +61,17 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     build_dir = os.path.join(PKG, "build_checked" if checked else "build")
     os.makedirs(build_dir, exist_ok=True)
     extra = ["-DKMD_CHECKS"] if checked else []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units compile concurrently (one nvcc process each)
+    from concurrent.futures import ThreadPoolExecutor
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for src, obj, cmd, r in results:
         log_lines.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
