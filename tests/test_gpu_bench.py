@@ -44,3 +44,14 @@ def test_default_mode_json_contract():
 def test_next_row_modes_json(mode):
     d = _run("--mode", mode, "--steps", "16", "--warmup", "3", "--height", "272", "--width", "480")
     assert d["value"] > 0 and 0 < d["roofline"]["frac"] < 1 and "workload" in d["config"]
+
+
+def test_bf16_mode_e2e_copies_bf16_inputs():
+    H, W = 272, 480
+    d = _run("--bf16", "--steps", "16", "--warmup", "3", "--height", str(H), "--width", str(W), "--e2e-steps", "3",
+             "--no-cpu-baseline")
+    e = d["e2e"]
+    assert "host_bf16" in e["path"] and e["value"] > 0
+    # radiance fp32 (3 planes) + importance and logits bf16 (6 + 6 planes)
+    assert e["h2d_bytes_per_step"] == H * W * (3 * 4 + 12 * 2)
+    assert e["d2h_bytes_per_step"] == H * W * 3 * 4
