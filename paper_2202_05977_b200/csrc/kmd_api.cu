@@ -80,14 +80,19 @@ bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
 }
 
 // Common launch path for whole frames and bands.
+// development switches / checked-build jitter seed (env KMD_DEBUG, read once)
+int debug_env() {
+    static const int dbg = [] { const char* e = getenv("KMD_DEBUG"); return e ? atoi(e) : 0; }();
+    return dbg;
+}
+
 kmd_status run_fused(kmd::FusedParams p, const kmd_config* cfg, cudaStream_t stream) {
     p.M = cfg->num_sizes;
     p.rmax = rmax_of(cfg);
     p.blend_is_logits = cfg->blend_is_logits;
     for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < cfg->num_sizes ? cfg->sizes[i] : 1;
     if (p.M == 1) p.blend = nullptr;  // softmax of one logit is 1 (reading R11)
-    static const int dbg = [] { const char* e = getenv("KMD_DEBUG"); return e ? atoi(e) : 0; }();
-    p.debug = dbg;
+    p.debug = debug_env();
     const size_t bplane = (size_t)p.buf_rows * p.W, oplane = (size_t)p.out_rows * p.W;
     const size_t esz = p.in16 ? 2 : 4;  // bytes per importance / logit element
     const int total = p.N;
@@ -760,6 +765,7 @@ kmd_status kmd_mr_decode_filter_fuse(const float* radiance, const float* const* 
                 p.row_base = 0; p.buf_rows = p.H; p.out_y0 = 0; p.out_rows = p.H;
                 const kmd_config& lc = cfg->level[l];
                 p.M = lc.num_sizes; p.rmax = rmax_of(&lc); p.blend_is_logits = lc.blend_is_logits;
+                p.debug = debug_env();
                 for (int i = 0; i < KMD_MAX_SIZES; ++i) p.sizes[i] = i < lc.num_sizes ? lc.sizes[i] : 1;
                 if (l < L - 1) {
                     p.cmb_coarse = f[l + 1];  // the combined next-coarser level (the coarsest: as filtered)

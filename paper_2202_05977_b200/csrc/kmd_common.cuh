@@ -22,9 +22,29 @@
             __trap();                                                                                \
         }                                                                                            \
     } while (0)
+// Scheduling jitter (checked builds only): with a nonzero seed (FusedParams
+// debug = env KMD_DEBUG, read once per process), every role of the TMA kernel
+// sleeps a pseudo-random 0-2 us at a quarter of its protocol points (before a
+// producer issue, a field job, a fusion step, a store), so the warps
+// interleave differently from run to run; a missing wait or an early slot
+// release then changes the output, which tests/test_gpu_checked.py compares
+// bit for bit with an unperturbed run.
+#define KMD_JITTER(seed, key) kmd_jitter((unsigned)(seed), (unsigned)(key))
+__device__ __forceinline__ void kmd_jitter(unsigned seed, unsigned key) {
+    if (seed) {
+        unsigned h = (key ^ seed) * 0x9E3779B1u ^ (blockIdx.x * 0x85EBCA77u) ^ (threadIdx.x >> 5) * 0xC2B2AE3Du;
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        if ((h & 3) == 0) __nanosleep(h >> 21);
+    }
+}
 #else
 #define KMD_CHECK(cond) \
     do {                \
+    } while (0)
+#define KMD_JITTER(seed, key) \
+    do {                      \
     } while (0)
 #endif
 

@@ -827,6 +827,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             tma_prefetch_3d(&tm_blend, pf.x0 - xalign<SP::IN16>(pf.x0), pf.y0 - p.out_y0, pf.n * M + i);
                     }
                 }
+                KMD_JITTER(p.debug, tl * 64 + 63);
                 IWAIT(0, mbar_wait(&sm.rad_empty[rb], ((tl / NRAD) & 1) ^ 1));
                 if (KMD_DBG(256)) {
                     mbar_arrive(&sm.rad_full[rb]);
@@ -837,6 +838,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 for (int i = 0; i < M; ++i) {
                     const int seq = tl * M + i, s = seq % NI;
+                    KMD_JITTER(p.debug, tl * 64 + i);
                     IWAIT(1, mbar_wait(&sm.in_empty[s], ((seq / NI) & 1) ^ 1));
                     if (KMD_DBG(128)) {
                         mbar_arrive(&sm.in_full[s]);
@@ -911,6 +913,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int si = seq % NI, sv = seq % NV;
                 Slot& sl = sm.slot[sv];
                 auto& in = sm.in[si];
+                KMD_JITTER(p.debug, 0x100000u + g);
                 IWAIT(3, mbar_wait(&sm.v_empty[sv], ((seq / NV) & 1) ^ 1));  // V slot free
                 IWAIT(4, mbar_wait(EPRE ? &sm.e_full[si] : &sm.in_full[si], (seq / NI) & 1));
                 const int R = (rpack >> (4 * i)) & 15;
@@ -1174,6 +1177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     bs = seq % NB; bph = (seq / NB) & 1;
                 }
                 epre(tl * M + ii + EPRE_AHEAD);
+                KMD_JITTER(p.debug, 0x200000u + tl * 16 + ii);
                 IWAIT(6, mbar_wait(&sm.v_full[vs], vph));
                 if (has_blend) IWAIT(7, mbar_wait(&sm.b_full[bs], bph));
                 IWAIT(12, if (!(KMD_DBG(64)) && active) fuse_job<BEXP ? FUSE_SOFTMAX_PRE : SP::MODE>(
@@ -1201,6 +1205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #ifdef KMD_INSTR
             const long long t_epi = clock64();
 #endif
+            KMD_JITTER(p.debug, 0x300000u + tl);
             IWAIT(9, fuse_bar());  // every fusion thread is done with the last V: it becomes the stage
             auto stage = stage_of(sm.slot[stage_slot]);
             const int gy = tc.y0 + ty;
@@ -1272,6 +1277,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             fence_proxy_async();
+            KMD_JITTER(p.debug, 0x400000u + tl);
             IWAIT(10, fuse_bar());
             if (tc.y0 >= p.out_y0) {
                 // TMA store; it clips the parts beyond W / out_rows.  (A TMA store
